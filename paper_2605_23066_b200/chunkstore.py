@@ -1,0 +1,870 @@
+"""Chunked n-d arrays: grid rules, the native chunk writer/reader, metadata merge.
+
+On-disk format (identical to the reference, ``chunkstore.py:1-14``): an array is a grid
+of write chunks aligned to shard boundaries, optionally subdivided into read chunks;
+a chunk payload is the raw little-endian row-major bytes of its box.  Two layouts:
+
+* per-leaf   — one object ``<prefix>/<leaf>/c.<i0>.<i1>…`` per write chunk;
+* aggregated — payloads appended to ``<prefix>/d/<file_id>`` data files (greedy flush when
+  the next payload would exceed the target), located through ``manifest.json``.
+
+What is B200-specific: chunk payloads are never materialised by Python.
+``ProcessArrayWriter`` turns every chunk into a descriptor (source device address, box,
+output file, offset) and the native engine packs strided boxes on the GPU, DMA's them
+into pinned slots and writes them with its own threads; ``ChunkReader.read_range`` and
+the load pipeline do the inverse.  The grid arithmetic, key names, manifest and metadata
+documents are host logic mirroring ``chunkstore.py:50-246, 249-305, 426-454, 603-690``.
+"""
+
+from __future__ import annotations
+
+import itertools
+import math
+from bisect import bisect_left
+from dataclasses import dataclass, field
+from typing import Any, Iterable, Iterator, Optional, Sequence
+
+import numpy as np
+
+from . import docio
+from .backend import Store
+from .dtypes import itemsize, numpy_dtype
+from .errors import (
+    AlignmentError,
+    ChunkStoreError,
+    ConsistencyError,
+    CorruptionError,
+    DuplicateChunkError,
+    MissingKeyError,
+)
+from .sharding import Range, segment_axis
+
+PER_LEAF = "per_leaf"
+AGGREGATED = "aggregated"
+LAYOUTS = (PER_LEAF, AGGREGATED)
+
+DEFAULT_TARGET_FILE_BYTES = 64 * 1024 * 1024
+
+ARRAY_METADATA_FILE = "array_metadata.json"
+MANIFEST_FILE = "manifest.json"
+DATA_DIR = "d"
+
+
+def _divides(part: int, whole: int) -> bool:
+    if whole == 0:
+        return part == 0
+    return part >= 1 and whole % part == 0
+
+
+@dataclass(frozen=True)
+class ChunkGrid:
+    """Write-chunk and read-subchunk shapes over one shard grid."""
+
+    shard_shape: tuple[int, ...]
+    write_chunk: tuple[int, ...]
+    read_chunk: tuple[int, ...]
+
+    def __post_init__(self):
+        for s, w, r in zip(self.shard_shape, self.write_chunk, self.read_chunk):
+            if not _divides(w, s):
+                raise ChunkStoreError(
+                    f"write chunk {self.write_chunk} does not subdivide shard {self.shard_shape}"
+                )
+            if not _divides(r, w):
+                raise ChunkStoreError(
+                    f"read chunk {self.read_chunk} does not subdivide write chunk {self.write_chunk}"
+                )
+
+
+@dataclass(frozen=True)
+class ArrayStorageMetadata:
+    global_shape: tuple[int, ...]
+    dtype: str
+    shard_shape: tuple[int, ...]
+    write_chunk: tuple[int, ...]
+    read_chunk: tuple[int, ...]
+    layout: str
+
+    def __post_init__(self):
+        if self.layout not in LAYOUTS:
+            raise ChunkStoreError(f"unknown layout {self.layout!r}")
+        if not _grid_consistent(self.global_shape, self.shard_shape):
+            raise ChunkStoreError(
+                f"shard {self.shard_shape} does not subdivide global {self.global_shape}"
+            )
+        ChunkGrid(self.shard_shape, self.write_chunk, self.read_chunk)
+        numpy_dtype(self.dtype)
+
+    @property
+    def rank(self) -> int:
+        return len(self.global_shape)
+
+    def chunk_counts(self) -> tuple[int, ...]:
+        return tuple(0 if g == 0 else g // w for g, w in zip(self.global_shape, self.write_chunk))
+
+    def total_chunks(self) -> int:
+        return math.prod(self.chunk_counts())
+
+    def chunk_nbytes(self) -> int:
+        return math.prod(self.write_chunk) * itemsize(self.dtype)
+
+    def to_json(self) -> dict:
+        return {
+            "global_shape": list(self.global_shape),
+            "dtype": self.dtype,
+            "shard_shape": list(self.shard_shape),
+            "write_chunk": list(self.write_chunk),
+            "read_chunk": list(self.read_chunk),
+            "layout": self.layout,
+        }
+
+    @classmethod
+    def from_json(cls, doc: dict) -> "ArrayStorageMetadata":
+        try:
+            return cls(
+                tuple(doc["global_shape"]), doc["dtype"], tuple(doc["shard_shape"]),
+                tuple(doc["write_chunk"]), tuple(doc["read_chunk"]), doc["layout"],
+            )
+        except (KeyError, TypeError) as exc:
+            raise CorruptionError(f"malformed array metadata: {exc}") from exc
+
+
+def _grid_consistent(global_shape: tuple[int, ...], part: tuple[int, ...]) -> bool:
+    return len(part) == len(global_shape) and all(
+        _divides(p, g) for p, g in zip(part, global_shape)
+    )
+
+
+def _smallest_prime_factor(n: int) -> int:
+    if n % 2 == 0:
+        return 2
+    f = 3
+    while f * f <= n:
+        if n % f == 0:
+            return f
+        f += 2
+    return n
+
+
+def choose_chunk_shape(shard_shape: tuple[int, ...], dtype: str, target_bytes: int) -> tuple[int, ...]:
+    """Read-chunk shape dividing ``shard_shape`` with at most ``target_bytes`` per chunk
+    when reachable.  Dims are reduced largest-first (ties: lowest index), halving while
+    even, else dividing by the smallest prime factor (``chunkstore.py:156-182``)."""
+    isz = itemsize(dtype)
+    if target_bytes < isz:
+        raise ChunkStoreError(f"target {target_bytes} B below element size {isz} B")
+    chunk = [int(s) for s in shard_shape]
+    if 0 in chunk:
+        return tuple(chunk)
+    for d in sorted(range(len(chunk)), key=lambda i: (-shard_shape[i], i)):
+        while chunk[d] > 1 and math.prod(chunk) * isz > target_bytes:
+            chunk[d] //= 2 if chunk[d] % 2 == 0 else _smallest_prime_factor(chunk[d])
+    return tuple(chunk)
+
+
+def derive_write_chunk(shard_shape: tuple[int, ...], n_segments: int) -> tuple[int, ...]:
+    """Write chunk aligned with ceil-division replica segmenting: the segment axis extent
+    becomes gcd(ceil(s/n), s) (``chunkstore.py:185-202``)."""
+    if n_segments <= 1 or not shard_shape or 0 in shard_shape:
+        return tuple(shard_shape)
+    axis = segment_axis(tuple(shard_shape))
+    s = shard_shape[axis]
+    chunk = list(shard_shape)
+    chunk[axis] = math.gcd(-(-s // n_segments), s)
+    return tuple(chunk)
+
+
+def coords_key(coords: tuple[int, ...]) -> str:
+    return ".".join(map(str, coords)) if coords else "0"
+
+
+def chunk_object_key(leaf_path: str, coords: tuple[int, ...]) -> str:
+    return f"{leaf_path}/c.{coords_key(coords)}"
+
+
+def _covering(ranges: tuple[Range, ...], steps: tuple[int, ...]) -> Iterator[tuple[int, ...]]:
+    """Grid coordinates (product order) of the cells meeting ``ranges``."""
+    spans = []
+    for (off, ext), step in zip(ranges, steps):
+        if ext == 0:
+            return
+        spans.append(range(off // step, (off + ext - 1) // step + 1))
+    yield from itertools.product(*spans)
+
+
+def _cell_ranges(coords: tuple[int, ...], steps: tuple[int, ...]) -> tuple[Range, ...]:
+    return tuple((c * s, s) for c, s in zip(coords, steps))
+
+
+def _intersect(a: tuple[Range, ...], b: tuple[Range, ...]) -> tuple[Range, ...] | None:
+    out = []
+    for (ao, ae), (bo, be) in zip(a, b):
+        lo, hi = max(ao, bo), min(ao + ae, bo + be)
+        if lo >= hi:
+            return None
+        out.append((lo, hi - lo))
+    return tuple(out)
+
+
+def _slab_is_contiguous(extents: tuple[int, ...], shape: tuple[int, ...]) -> bool:
+    """Is a leading box of ``extents`` one contiguous run inside ``shape``?"""
+    partial = [d for d, (e, s) in enumerate(zip(extents, shape)) if e != s]
+    if not partial:
+        return True
+    return all(extents[d] == 1 for d in range(partial[-1]))
+
+
+def _strides(shape: tuple[int, ...]) -> tuple[int, ...]:
+    out = [1] * len(shape)
+    for d in range(len(shape) - 2, -1, -1):
+        out[d] = out[d + 1] * shape[d + 1]
+    return tuple(out)
+
+
+def box_is_contiguous(shape: Sequence[int], off: Sequence[int], ext: Sequence[int]) -> bool:
+    """Is box (off, ext) a single byte run of a row-major array of ``shape``?"""
+    dims = [d for d, e in enumerate(ext) if e > 1]
+    if not dims:
+        return True
+    return all(ext[d] == shape[d] for d in range(dims[0] + 1, len(shape)))
+
+
+def box_flat_offset(shape: Sequence[int], off: Sequence[int]) -> int:
+    return sum(o * s for o, s in zip(off, _strides(tuple(shape))))
+
+
+class AggregatedManifest:
+    """Sorted chunk key -> (file_id, offset, length) index of aggregated data files."""
+
+    def __init__(self, entries: dict[str, tuple[int, int, int]], target_file_bytes: int):
+        self._keys = sorted(entries)
+        self._locs = [tuple(entries[k]) for k in self._keys]
+        self.target_file_bytes = target_file_bytes
+        self._validate()
+
+    def _validate(self) -> None:
+        spans: dict[int, list[tuple[int, int]]] = {}
+        for fid, off, length in self._locs:
+            if off < 0 or length < 0:
+                raise CorruptionError("negative manifest byte range")
+            spans.setdefault(fid, []).append((off, length))
+        for fid, ranges in spans.items():
+            ranges.sort()
+            for (o1, l1), (o2, _) in zip(ranges, ranges[1:]):
+                if o1 + l1 > o2:
+                    raise CorruptionError(f"overlapping byte ranges in data file {fid}")
+
+    def __len__(self) -> int:
+        return len(self._keys)
+
+    def keys(self) -> list[str]:
+        return list(self._keys)
+
+    def lookup(self, key: str) -> tuple[int, int, int]:
+        i = bisect_left(self._keys, key)
+        if i == len(self._keys) or self._keys[i] != key:
+            raise MissingKeyError(f"chunk key {key!r} not in manifest")
+        return self._locs[i]
+
+    def to_json(self) -> dict:
+        return {
+            "target_file_bytes": self.target_file_bytes,
+            "entries": {k: list(v) for k, v in zip(self._keys, self._locs)},
+        }
+
+    @classmethod
+    def from_json(cls, doc: dict) -> "AggregatedManifest":
+        try:
+            entries = {k: (int(f), int(o), int(l)) for k, (f, o, l) in doc["entries"].items()}
+            return cls(entries, int(doc["target_file_bytes"]))
+        except (KeyError, TypeError, ValueError) as exc:
+            raise CorruptionError(f"malformed manifest: {exc}") from exc
+
+
+# -- device regions ---------------------------------------------------------------------
+
+
+@dataclass
+class DeviceRegion:
+    """Where the values of one box live on a GPU: ``tensor`` (contiguous, row-major)
+    holds the box at offset ``origin`` (per-dimension).  A shard, a global array and a
+    packed snapshot buffer are all DeviceRegions — no copy is made to describe a box."""
+
+    tensor: Any
+    origin: tuple[int, ...]
+    gpu: int
+
+    @property
+    def shape(self) -> tuple[int, ...]:
+        return tuple(int(s) for s in self.tensor.shape)
+
+    @property
+    def address(self) -> int:
+        return int(self.tensor.data_ptr())
+
+
+def as_device_region(values: Any, extents: tuple[int, ...], dtype: str, gpu: int | None = None) -> DeviceRegion:
+    """Accept a DeviceRegion, a torch CUDA tensor of exactly ``extents`` or a host numpy
+    array (uploaded once — the compatibility path of ``write_array`` callers that pass
+    numpy boxes)."""
+    import torch
+
+    from .dtypes import torch_dtype
+
+    if isinstance(values, DeviceRegion):
+        return values
+    if isinstance(values, torch.Tensor):
+        t = values
+        if not t.is_cuda:
+            dev = torch.device("cuda", gpu if gpu is not None else torch.cuda.current_device())
+            t = t.to(dev)
+    else:
+        from .treemodel import _host_storage
+
+        host = np.ascontiguousarray(_host_storage(values, dtype))
+        dev = torch.device("cuda", gpu if gpu is not None else torch.cuda.current_device())
+        t = torch.from_numpy(host.view(np.uint8).reshape(-1)).to(dev)
+        t = t.view(torch_dtype(dtype)).reshape(host.shape) if host.size else torch.empty(
+            host.shape, dtype=torch_dtype(dtype), device=dev)
+    if tuple(t.shape) != tuple(extents):
+        raise AlignmentError(f"shard buffer shape {tuple(t.shape)} does not match extents {extents}")
+    t = t.contiguous()
+    return DeviceRegion(t, (0,) * len(extents), t.device.index)
+
+
+def _fill_box(rec: np.ndarray, base: int, shape: Sequence[int], off: Sequence[int]) -> None:
+    rec["base"] = base
+    rank = len(shape)
+    rec["shape"][:rank] = shape
+    rec["off"][:rank] = off
+
+
+# -- writer ---------------------------------------------------------------------------------
+
+
+@dataclass
+class _PendingChunk:
+    key: str          # full storage key of the output (chunk object, or data file)
+    region: DeviceRegion
+    box_off: tuple[int, ...]   # chunk origin inside region.tensor
+    ext: tuple[int, ...]
+    itemsize: int
+    nbytes: int
+    file_off: int
+
+
+class ProcessArrayWriter:
+    """Writes one process's chunks under ``<prefix>`` (``chunkstore.py:307-454``).
+
+    ``write_array`` only plans (keys, file offsets, duplicate checks); the bytes move in
+    ``flush`` — one native engine call for all arrays of the process — which ``finish``
+    runs before writing the manifest and ``array_metadata.json``.  Op order on the
+    backend is the reference's: chunk puts in write order, then manifest, then metadata.
+    """
+
+    def __init__(self, store: Store, prefix: str, layout: str,
+                 target_file_bytes: int = DEFAULT_TARGET_FILE_BYTES, *, engine_cfg=None,
+                 concurrent: int = 1):
+        if layout not in LAYOUTS:
+            raise ChunkStoreError(f"unknown layout {layout!r}")
+        self._store = store
+        self._prefix = prefix.rstrip("/")
+        self._layout = layout
+        self._target = target_file_bytes
+        self._metas: dict[str, ArrayStorageMetadata] = {}
+        self._shardings: dict[str, Optional[dict]] = {}
+        self._chunks: dict[str, set[str]] = {}
+        self._manifest_entries: dict[str, tuple[int, int, int]] = {}
+        self._pending: list[_PendingChunk] = []
+        self._fid = 0        # aggregated: current data file id
+        self._cur_fill = 0   # aggregated: bytes already assigned to it
+        self._finished = False
+        self._engine_cfg = engine_cfg
+        self._concurrent = concurrent
+        self.stats = None
+
+    def declare_array(self, leaf_path: str, meta: ArrayStorageMetadata,
+                      sharding_descriptor: dict | None = None) -> None:
+        if meta.layout != self._layout:
+            raise ChunkStoreError("array layout differs from writer layout")
+        known = self._metas.get(leaf_path)
+        if known is not None and known != meta:
+            raise ConsistencyError(f"conflicting metadata for {leaf_path!r}")
+        self._metas[leaf_path] = meta
+        self._shardings.setdefault(leaf_path, sharding_descriptor)
+        self._chunks.setdefault(leaf_path, set())
+
+    def write_array(self, leaf_path: str, shards: Iterable[tuple[tuple[Range, ...], Any]],
+                    meta: ArrayStorageMetadata, sharding_descriptor: dict | None = None) -> list[str]:
+        """Plan whole write chunks of each (ranges, values) piece; returns the keys the
+        chunks will be stored under.  ``values`` is a DeviceRegion / CUDA tensor / numpy
+        box exactly covering ``ranges``."""
+        self.declare_array(leaf_path, meta, sharding_descriptor)
+        isz = itemsize(meta.dtype)
+        keys = []
+        for ranges, values in shards:
+            ranges = tuple((int(o), int(e)) for o, e in ranges)
+            if len(ranges) != meta.rank:
+                raise AlignmentError(f"rank mismatch for {leaf_path!r}")
+            for (off, ext), w, g in zip(ranges, meta.write_chunk, meta.global_shape):
+                if off < 0 or off + ext > g:
+                    raise AlignmentError(
+                        f"range ({off}, {ext}) outside global extent {g} for {leaf_path!r}"
+                    )
+                if ext and (off % w or ext % w):
+                    raise AlignmentError(
+                        f"range ({off}, {ext}) of {leaf_path!r} not aligned to write chunk "
+                        f"{meta.write_chunk}"
+                    )
+            extents = tuple(e for _, e in ranges)
+            region = as_device_region(values, extents, meta.dtype)
+            if not isinstance(values, DeviceRegion) and region.shape != extents:
+                raise AlignmentError(
+                    f"shard buffer shape {region.shape} does not match ranges {ranges} "
+                    f"for {leaf_path!r}"
+                )
+            nbytes = math.prod(meta.write_chunk) * isz
+            for coords in _covering(ranges, meta.write_chunk):
+                box_off = tuple(
+                    o + c * w - r0
+                    for o, c, w, (r0, _) in zip(region.origin, coords, meta.write_chunk, ranges)
+                )
+                keys.append(self._plan_chunk(leaf_path, coords, region, box_off, meta.write_chunk,
+                                             isz, nbytes))
+        return keys
+
+    def _plan_chunk(self, leaf_path, coords, region, box_off, ext, isz, nbytes) -> str:
+        ck = coords_key(coords)
+        seen = self._chunks[leaf_path]
+        if ck in seen:
+            raise DuplicateChunkError(f"chunk {ck} of {leaf_path!r} written twice")
+        seen.add(ck)
+        rel = chunk_object_key(leaf_path, coords)
+        if self._layout == PER_LEAF:
+            key = f"{self._prefix}/{rel}"
+            self._pending.append(_PendingChunk(key, region, box_off, ext, isz, nbytes, 0))
+            return key
+        # Greedy packing (chunkstore.py:409-417): a new file starts when the current one
+        # is non-empty and the payload would push it past the target.
+        if self._cur_fill and self._cur_fill + nbytes > self._target:
+            self._fid += 1
+            self._cur_fill = 0
+        fid = self._fid
+        self._manifest_entries[rel] = (fid, self._cur_fill, nbytes)
+        key = f"{self._prefix}/{DATA_DIR}/{fid}"
+        self._pending.append(_PendingChunk(key, region, box_off, ext, isz, nbytes, self._cur_fill))
+        self._cur_fill += nbytes
+        return key
+
+    # -- execution ---------------------------------------------------------------------------
+
+    def flush(self) -> None:
+        """Move every planned chunk to storage (one native engine call)."""
+        pending, self._pending = self._pending, []
+        if not pending:
+            return
+        self.stats = execute_writes(self._store, pending, self._engine_cfg, self._concurrent)
+
+    def finish(self) -> dict:
+        """Flush chunks, then write the manifest (aggregated) and the per-process
+        metadata document; returns the document."""
+        if self._finished:
+            raise ChunkStoreError("writer already finished")
+        self._finished = True
+        self.flush()
+        if self._layout == AGGREGATED:
+            manifest = AggregatedManifest(self._manifest_entries, self._target)
+            self._store.put(f"{self._prefix}/{MANIFEST_FILE}", docio.dumps_canonical(manifest.to_json()))
+        doc = {
+            "format_version": 1,
+            "layout": self._layout,
+            "arrays": {
+                leaf: {
+                    **meta.to_json(),
+                    "sharding": self._shardings.get(leaf),
+                    "chunks": sorted(self._chunks[leaf]),
+                }
+                for leaf, meta in self._metas.items()
+            },
+        }
+        self._store.put(f"{self._prefix}/{ARRAY_METADATA_FILE}", docio.dumps_canonical(doc))
+        return doc
+
+
+def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, concurrent: int = 1):
+    """Run planned chunk writes through the native engine.
+
+    Outputs are the distinct keys in first-appearance order (one per chunk, or one per
+    aggregated data file).  The backend admits the puts in that order (fault plan,
+    payload gate), the engine writes them, the backend records them.
+    """
+    from . import native
+
+    out_keys: list[str] = []
+    out_index: dict[str, int] = {}
+    sizes: list[int] = []
+    for p in pending:
+        i = out_index.get(p.key)
+        if i is None:
+            i = out_index[p.key] = len(out_keys)
+            out_keys.append(p.key)
+            sizes.append(0)
+        sizes[i] = max(sizes[i], p.file_off + p.nbytes)
+    backend = store.backend
+    store.sched_point()
+    n_ok, err = backend.admit_bulk("put", out_keys)
+    if n_ok < len(out_keys):
+        allowed = set(range(n_ok))
+        keep = [p for p in pending if out_index[p.key] in allowed]
+        out_keys, sizes = out_keys[:n_ok], sizes[:n_ok]
+        pending = keep
+    cfg = engine_cfg or native.EngineConfig()
+    root = backend.native_root()
+    stats = None
+    if pending:
+        items = np.zeros(len(pending), native.WRITE_ITEM)
+        for j, p in enumerate(pending):
+            rec = items[j]
+            _fill_box(rec["src"], p.region.address, p.region.shape, p.box_off)
+            rank = len(p.ext)
+            rec["ext"][:rank] = p.ext
+            rec["rank"] = rank
+            rec["itemsize"] = p.itemsize
+            rec["file"] = out_index[p.key]
+            rec["device"] = p.region.gpu
+            rec["file_off"] = p.file_off
+        outputs = np.zeros(len(out_keys), native.OUTPUT)
+        outputs["size"] = sizes
+        host_bufs: list[np.ndarray] = []
+        if root is not None:
+            paths = native.PathTable([backend.path_of(k) for k in out_keys])
+            outputs["path"] = paths.pointers
+        else:
+            for i, size in enumerate(sizes):
+                buf = np.empty(size, np.uint8)
+                host_bufs.append(buf)
+                outputs[i]["host"] = buf.ctypes.data if size else 0
+        with native.engine_lease(cfg, concurrent) as eng:
+            stats = eng.save(items, outputs)
+        if root is not None:
+            backend.record_bulk(store.identity, "put", out_keys, [0] * len(out_keys), sizes)
+        else:
+            # Non-filesystem backends receive ordinary puts of the produced bytes; the
+            # admission above already counted them, so go straight to the backend op.
+            for key, buf in zip(out_keys, host_bufs):
+                data = buf.tobytes()
+                with backend._lock:
+                    backend._put(key, data)
+                    backend._record(store.identity, "put", key, 0, len(data))
+    if err is not None:
+        raise err
+    return stats
+
+
+# -- reader -----------------------------------------------------------------------------------
+
+
+@dataclass
+class ReadStats:
+    bytes_requested: int = 0
+    bytes_loaded: int = 0
+
+
+@dataclass
+class Fetch:
+    """One contiguous byte range of a stored chunk and the box it holds."""
+
+    key: str                      # storage key read
+    op: str                       # "get" | "get_range"
+    file_off: int
+    nbytes: int
+    origin: tuple[int, ...]       # global origin of the fetched box
+    shape: tuple[int, ...]        # box shape (write chunk or read chunk)
+    whole_file: bool
+
+
+def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMetadata,
+                 requests: Sequence[tuple[Range, ...]]) -> list[Fetch]:
+    """Minimal fetch list covering the union of ``requests`` for one array
+    (``chunkstore.py:507-578``): per covering write chunk, the whole chunk when every
+    subchunk is needed or subchunks are not contiguous in it, else one byte-range fetch
+    per needed subchunk."""
+    w, r = meta.write_chunk, meta.read_chunk
+    isz = itemsize(meta.dtype)
+    subs_per = tuple(wi // ri for wi, ri in zip(w, r))
+    n_subs = math.prod(subs_per)
+    contiguous = _slab_is_contiguous(r, w)
+    wstrides = _strides(w)
+    chunks: dict[tuple[int, ...], set[tuple[int, ...]]] = {}
+    order: list[tuple[int, ...]] = []
+    for ranges in requests:
+        if any(e == 0 for _, e in ranges):
+            continue
+        for coords in _covering(ranges, w):
+            hit = _intersect(ranges, _cell_ranges(coords, w))
+            if hit is None:
+                continue
+            subs = chunks.get(coords)
+            if subs is None:
+                subs = chunks[coords] = set()
+                order.append(coords)
+            subs.update(_covering(hit, r))
+    locations = entry["chunks"]
+    out: list[Fetch] = []
+    chunk_bytes = math.prod(w) * isz
+    sub_bytes = math.prod(r) * isz
+    for coords in order:
+        ck = coords_key(coords)
+        loc = locations.get(ck)
+        if loc is None:
+            raise CorruptionError(f"chunk {ck} of {leaf_path!r} missing from merged index")
+        if "f" in loc:
+            key = f"{prefix}/process_{loc['p']}/{DATA_DIR}/{loc['f']}"
+            base, op, whole = int(loc["o"]), "get_range", False
+        else:
+            key = f"{prefix}/process_{loc['p']}/" + chunk_object_key(leaf_path, coords)
+            base, op, whole = 0, "get", True
+        needed = chunks[coords]
+        origin = tuple(c * wi for c, wi in zip(coords, w))
+        if len(needed) == n_subs or not contiguous:
+            out.append(Fetch(key, op, base, chunk_bytes, origin, tuple(w), whole))
+            continue
+        for sub in sorted(needed):
+            rel = tuple(s - c * n for s, c, n in zip(sub, coords, subs_per))
+            first = sum(rc * ri * st for rc, ri, st in zip(rel, r, wstrides))
+            sub_origin = tuple(s * ri for s, ri in zip(sub, r))
+            out.append(Fetch(key, "get_range", base + first * isz, sub_bytes, sub_origin,
+                             tuple(r), False))
+    return out
+
+
+class ChunkReader:
+    """Reads array ranges of a finalized checkpoint through its merged index."""
+
+    def __init__(self, store: Store, ckpt_prefix: str, merged_index: dict, *, gpu: int | None = None,
+                 engine_cfg=None):
+        self._store = store
+        self._prefix = ckpt_prefix.rstrip("/")
+        self._arrays = merged_index["arrays"]
+        self._gpu = gpu
+        self._engine_cfg = engine_cfg
+
+    def metadata_for(self, leaf_path: str) -> ArrayStorageMetadata:
+        if leaf_path not in self._arrays:
+            raise CorruptionError(f"leaf {leaf_path!r} missing from merged index")
+        return ArrayStorageMetadata.from_json(self._arrays[leaf_path])
+
+    def read_range(self, leaf_path: str, ranges: tuple[Range, ...]):
+        """The box ``ranges`` of ``leaf_path`` as a fresh CUDA tensor (loading the
+        minimal set of read chunks), plus byte stats; ``.cpu()`` it for host bytes."""
+        import torch
+
+        from .dtypes import torch_dtype
+
+        meta = self.metadata_for(leaf_path)
+        isz = itemsize(meta.dtype)
+        ranges = tuple((int(o), int(e)) for o, e in ranges)
+        if len(ranges) != meta.rank:
+            raise ChunkStoreError(f"rank mismatch reading {leaf_path!r}")
+        for (off, ext), g in zip(ranges, meta.global_shape):
+            if off < 0 or ext < 0 or off + ext > g:
+                raise ChunkStoreError(f"range ({off}, {ext}) outside global extent {g}")
+        extents = tuple(e for _, e in ranges)
+        gpu = self._gpu if self._gpu is not None else torch.cuda.current_device()
+        out = torch.empty(extents, dtype=torch_dtype(meta.dtype), device=torch.device("cuda", gpu))
+        stats = ReadStats(bytes_requested=math.prod(extents) * isz)
+        if 0 in extents:
+            return out, stats
+        fetches = plan_fetches(self._prefix, leaf_path, self._arrays[leaf_path], meta, [ranges])
+        dest = Destination(gpu, out.data_ptr(), ranges, isz)
+        items = [FetchItem(f, gpu, [dest]) for f in fetches]
+        execute_reads(self._store, items, self._engine_cfg)
+        stats.bytes_loaded = sum(f.nbytes for f in fetches)
+        return out, stats
+
+
+# -- restore execution ------------------------------------------------------------------------
+
+
+@dataclass
+class Destination:
+    """A target box on a GPU: the tensor at ``address`` holds global box ``ranges``."""
+
+    gpu: int
+    address: int
+    ranges: tuple[Range, ...]
+    itemsize: int
+
+
+@dataclass
+class FetchItem:
+    fetch: Fetch
+    reader_gpu: int
+    consumers: list[Destination] = field(default_factory=list)
+
+
+def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurrent: int = 1):
+    """Fetch every item once onto its reader GPU and scatter it into every consumer
+    (local or peer GPUs).  Admission / recording of the get ops as in execute_writes."""
+    from . import native
+
+    if not items:
+        return None
+    backend = store.backend
+    keys = [it.fetch.key for it in items]
+    store.sched_point()
+    n_ok, err = backend.admit_bulk("get", keys)
+    items = items[:n_ok]
+    root = backend.native_root()
+    input_index: dict[str, int] = {}
+    input_keys: list[str] = []
+    for it in items:
+        if it.fetch.key not in input_index:
+            input_index[it.fetch.key] = len(input_keys)
+            input_keys.append(it.fetch.key)
+    inputs = np.zeros(len(input_keys), native.INPUT)
+    keep_alive = []
+    if root is not None:
+        paths = native.PathTable([backend.path_of(k) for k in input_keys])
+        keep_alive.append(paths)
+        inputs["path"] = paths.pointers
+        try:
+            inputs["size"] = [backend._size(k) for k in input_keys]
+        except MissingKeyError:
+            raise
+    else:
+        for i, k in enumerate(input_keys):
+            with backend._lock:
+                data = backend._get(k)
+            arr = np.frombuffer(data, np.uint8)
+            keep_alive.append(arr)
+            inputs[i]["host"] = arr.ctypes.data if arr.size else 0
+            inputs[i]["size"] = arr.size
+    for it in items:
+        size = int(inputs[input_index[it.fetch.key]]["size"])
+        if it.fetch.file_off + it.fetch.nbytes > size:
+            from .errors import BackendError
+
+            raise BackendError(
+                f"range [{it.fetch.file_off}, {it.fetch.file_off + it.fetch.nbytes}) outside key "
+                f"{it.fetch.key!r} of size {size}"
+            )
+        if it.fetch.whole_file and size != it.fetch.nbytes:
+            raise CorruptionError(
+                f"chunk object {it.fetch.key!r} has {size} bytes, expected {it.fetch.nbytes}"
+            )
+    ritems = np.zeros(len(items), native.READ_ITEM)
+    copies_list = []
+    for j, it in enumerate(items):
+        f = it.fetch
+        rec = ritems[j]
+        rec["input"] = input_index[f.key]
+        rec["device"] = it.reader_gpu
+        rec["in_off"] = f.file_off
+        rec["nbytes"] = f.nbytes
+        fetched = tuple(zip(f.origin, f.shape))
+        direct = None
+        for d in it.consumers:
+            if d.gpu != it.reader_gpu:
+                continue
+            inside = all(
+                do <= fo and fo + fe <= do + de for (fo, fe), (do, de) in zip(fetched, d.ranges)
+            )
+            if not inside:
+                continue
+            dshape = tuple(e for _, e in d.ranges)
+            doff = tuple(fo - do for (fo, _), (do, _) in zip(fetched, d.ranges))
+            if box_is_contiguous(dshape, doff, f.shape):
+                direct = d
+                rec["direct_dst"] = d.address + box_flat_offset(dshape, doff) * d.itemsize
+                break
+        first = len(copies_list)
+        for d in it.consumers:
+            if d is direct:
+                continue
+            hit = _intersect(fetched, d.ranges)
+            if hit is None:
+                continue
+            c = np.zeros((), native.COPY)
+            rank = len(f.shape)
+            _fill_box(c["src"], 0, f.shape, tuple(h - o for (h, _), o in zip(hit, f.origin)))
+            _fill_box(c["dst"], d.address, tuple(e for _, e in d.ranges),
+                      tuple(h - o for (h, _), (o, _) in zip(hit, d.ranges)))
+            c["ext"][:rank] = [e for _, e in hit]
+            c["rank"] = rank
+            c["itemsize"] = d.itemsize
+            copies_list.append(c)
+        rec["first_copy"] = first
+        rec["n_copies"] = len(copies_list) - first
+    copies = np.array(copies_list, native.COPY) if copies_list else np.zeros(0, native.COPY)
+    cfg = engine_cfg or native.EngineConfig()
+    with native.engine_lease(cfg, concurrent) as eng:
+        stats = eng.load(ritems, inputs, copies)
+    backend.record_bulk(
+        store.identity, [it.fetch.op for it in items], [it.fetch.key for it in items],
+        [it.fetch.nbytes for it in items], [0] * len(items),
+    )
+    if err is not None:
+        raise err
+    return stats
+
+
+# -- metadata merge ---------------------------------------------------------------------------
+
+
+def merge_process_indices(store: Store, ckpt_prefix: str, process_count: int) -> dict:
+    """Merged index from the per-process documents (``chunkstore.py:603-690``): checks
+    that processes agree on every array, no chunk is claimed twice, and every grid is
+    complete; payload bytes are never read."""
+    prefix = ckpt_prefix.rstrip("/")
+    layout: str | None = None
+    arrays: dict[str, dict] = {}
+    metas: dict[str, ArrayStorageMetadata] = {}
+    leaf_sets: list[set[str]] = []
+    for p in range(process_count):
+        pdir = f"{prefix}/process_{p}"
+        try:
+            raw = store.get(f"{pdir}/{ARRAY_METADATA_FILE}")
+        except MissingKeyError:
+            raise ConsistencyError(f"missing array metadata for process {p}") from None
+        doc = docio.loads(raw, what=f"process {p} array metadata")
+        if layout is None:
+            layout = doc.get("layout")
+        elif doc.get("layout") != layout:
+            raise ConsistencyError(f"process {p} layout {doc.get('layout')!r} != {layout!r}")
+        manifest = None
+        if layout == AGGREGATED:
+            try:
+                raw = store.get(f"{pdir}/{MANIFEST_FILE}")
+            except MissingKeyError:
+                raise ConsistencyError(f"missing manifest for process {p}") from None
+            manifest = AggregatedManifest.from_json(docio.loads(raw, what=f"process {p} manifest"))
+        entries = doc.get("arrays", {})
+        leaf_sets.append(set(entries))
+        for leaf, entry in entries.items():
+            meta = ArrayStorageMetadata.from_json(entry)
+            if leaf not in metas:
+                metas[leaf] = meta
+                arrays[leaf] = {**meta.to_json(), "sharding": entry.get("sharding"), "chunks": {}}
+            elif metas[leaf] != meta:
+                raise ConsistencyError(f"process {p} disagrees on storage metadata for {leaf!r}")
+            elif arrays[leaf]["sharding"] != entry.get("sharding"):
+                raise ConsistencyError(f"process {p} disagrees on sharding for {leaf!r}")
+            located = arrays[leaf]["chunks"]
+            for ck in entry.get("chunks", []):
+                if ck in located:
+                    raise DuplicateChunkError(
+                        f"chunk {ck} of {leaf!r} claimed by processes {located[ck]['p']} and {p}"
+                    )
+                loc: dict = {"p": p}
+                if manifest is not None:
+                    fid, off, length = manifest.lookup(f"{leaf}/c.{ck}")
+                    loc.update({"f": fid, "o": off, "l": length})
+                located[ck] = loc
+    if any(s != set(arrays) for s in leaf_sets):
+        raise ConsistencyError("processes disagree on the array leaf set")
+    for leaf, entry in arrays.items():
+        expected = metas[leaf].total_chunks()
+        if len(entry["chunks"]) != expected:
+            raise ConsistencyError(f"{leaf!r} has {len(entry['chunks'])} of {expected} chunks")
+    return {"format_version": 1, "layout": layout or PER_LEAF, "arrays": arrays}

@@ -1,0 +1,1124 @@
+// libtvgpu I/O engine: the save and restore pipelines between HBM and storage.
+//
+// Save (tv_engine_save) — replaces SaveSession.write_phase → ProcessArrayWriter
+// (chunkstore.py:352-454) → FilesystemBackend._put (backend.py:398-403):
+//   producer (caller thread) walks the chunk payloads in file order and fills a ring of
+//   pinned host slots: a payload that is one contiguous byte range of its device array
+//   is DMA'd straight from HBM (no kernel), a strided box is first packed by the
+//   box-copy kernel into device staging and then DMA'd; every slot gets a CUDA event.
+//   Storage threads take filled slots, wait for their event, pwrite the bytes at their
+//   file offsets, and commit a file (<path>.partial → rename) when its last byte lands.
+//   D2H of slot k+1.. overlaps the writes of slot k; n_threads files are written at once.
+//
+// Restore (tv_engine_load) — replaces ChunkReader.read_range (chunkstore.py:507-593) and
+// _execute_reads/_assemble (load_pipeline.py:406-493):
+//   reader threads pread byte ranges into pinned slots and issue the H2D themselves,
+//   either straight into the destination shard (contiguous destination) or into device
+//   staging; when the last piece of an item has landed, the same thread launches the
+//   item's box copies (unpack / reshard scatter), whose destinations may be other GPUs
+//   (NVLink P2P or IPC-mapped) — the read-once fan-out.
+
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <sys/types.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "tv_internal.h"
+
+namespace tv {
+
+namespace {
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+std::string errno_msg(const std::string& what, const std::string& path) {
+  return what + " " + path + ": " + std::strerror(errno);
+}
+
+// ---- small concurrency helpers -----------------------------------------------------
+
+template <typename T>
+class Queue {
+ public:
+  void push(T v) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      q_.push_back(std::move(v));
+    }
+    cv_.notify_one();
+  }
+  bool pop(T& out) {  // false when closed and drained
+    std::unique_lock<std::mutex> g(m_);
+    cv_.wait(g, [&] { return closed_ || !q_.empty(); });
+    if (q_.empty()) return false;
+    out = std::move(q_.front());
+    q_.pop_front();
+    return true;
+  }
+  void close() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      closed_ = true;
+    }
+    cv_.notify_all();
+  }
+
+ private:
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::deque<T> q_;
+  bool closed_ = false;
+};
+
+struct ErrorSlot {
+  std::mutex m;
+  std::atomic<bool> failed{false};
+  int code = TV_OK;
+  std::string msg;
+  void set(int c, const std::string& s) {
+    std::lock_guard<std::mutex> g(m);
+    if (!failed.load()) {
+      code = c;
+      msg = s;
+      failed.store(true);
+    }
+  }
+};
+
+// mkdir -p with a cache of directories known to exist.
+class DirMaker {
+ public:
+  bool ensure(const std::string& dir, std::string& err) {
+    if (dir.empty()) return true;
+    {
+      std::lock_guard<std::mutex> g(m_);
+      if (done_.count(dir)) return true;
+    }
+    std::string cur;
+    size_t pos = 0;
+    while (pos != std::string::npos) {
+      pos = dir.find('/', pos + 1);
+      cur = dir.substr(0, pos);
+      if (cur.empty()) continue;
+      if (mkdir(cur.c_str(), 0777) != 0 && errno != EEXIST) {
+        err = errno_msg("mkdir", cur);
+        return false;
+      }
+    }
+    std::lock_guard<std::mutex> g(m_);
+    done_.insert(dir);
+    return true;
+  }
+
+ private:
+  std::mutex m_;
+  std::unordered_set<std::string> done_;
+};
+
+std::string parent_of(const std::string& path) {
+  size_t p = path.rfind('/');
+  return p == std::string::npos ? std::string() : path.substr(0, p);
+}
+
+// ---- per-device resources -------------------------------------------------------------
+
+// Uploads CopyJob tables to the device through a pinned ring; a region is reused only
+// after the kernel that read it has completed (event).
+class JobUploader {
+ public:
+  explicit JobUploader(int device) : device_(device) {}
+  ~JobUploader() {
+    cudaSetDevice(device_);
+    for (auto& r : inflight_) cudaEventDestroy(r.ev);
+    for (auto ev : free_events_) cudaEventDestroy(ev);
+    if (host_) cudaFreeHost(host_);
+    if (dev_) cudaFree(dev_);
+  }
+  // Copies `jobs`, launches the kernel, retires the region with an event.
+  int run(std::vector<CopyJob>& jobs, cudaStream_t stream, int64_t* launches) {
+    if (jobs.empty()) return TV_OK;
+    const int64_t total_units = plan_units(jobs);
+    const size_t bytes = jobs.size() * sizeof(CopyJob);
+    std::lock_guard<std::mutex> g(m_);
+    if (bytes > cap_) {
+      // Grow (rare): drain everything, reallocate.
+      for (auto& r : inflight_) {
+        cudaEventSynchronize(r.ev);
+        free_events_.push_back(r.ev);
+      }
+      inflight_.clear();
+      if (host_) cudaFreeHost(host_);
+      if (dev_) cudaFree(dev_);
+      cap_ = std::max<size_t>(bytes * 2, 1 << 20);
+      TV_CUDA_CHECK(cudaHostAlloc(&host_, cap_, cudaHostAllocDefault));
+      TV_CUDA_CHECK(cudaMalloc(&dev_, cap_));
+      head_ = 0;
+    }
+    if (head_ + bytes > cap_) head_ = 0;
+    // Wait for in-flight regions overlapping [head_, head_+bytes).
+    for (auto it = inflight_.begin(); it != inflight_.end();) {
+      bool overlap = it->off < head_ + bytes && head_ < it->off + it->len;
+      if (overlap || cudaEventQuery(it->ev) == cudaSuccess) {
+        TV_CUDA_CHECK(cudaEventSynchronize(it->ev));
+        free_events_.push_back(it->ev);
+        it = inflight_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    std::memcpy(host_ + head_, jobs.data(), bytes);
+    TV_CUDA_CHECK(cudaMemcpyAsync(dev_ + head_, host_ + head_, bytes, cudaMemcpyHostToDevice,
+                                  stream));
+    TV_CUDA_CHECK(launch_copy_jobs(reinterpret_cast<const CopyJob*>(dev_ + head_),
+                                   (int)jobs.size(), total_units, stream));
+    cudaEvent_t ev;
+    if (free_events_.empty()) {
+      TV_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    } else {
+      ev = free_events_.back();
+      free_events_.pop_back();
+    }
+    TV_CUDA_CHECK(cudaEventRecord(ev, stream));
+    inflight_.push_back({head_, bytes, ev});
+    head_ += (bytes + 255) & ~size_t(255);
+    if (launches) ++*launches;
+    return TV_OK;
+  }
+
+ private:
+  struct Region {
+    size_t off, len;
+    cudaEvent_t ev;
+  };
+  int device_;
+  std::mutex m_;
+  char* host_ = nullptr;
+  char* dev_ = nullptr;
+  size_t cap_ = 0, head_ = 0;
+  std::deque<Region> inflight_;
+  std::vector<cudaEvent_t> free_events_;
+};
+
+// First-fit allocator over one device staging buffer; frees are deferred to events.
+class StagingPool {
+ public:
+  StagingPool(int device, int64_t bytes) : device_(device), cap_(bytes) {}
+  ~StagingPool() {
+    cudaSetDevice(device_);
+    for (auto& p : pending_) cudaEventDestroy(p.ev);
+    if (base_) cudaFree(base_);
+  }
+  int init() {
+    if (base_ || cap_ == 0) return TV_OK;
+    TV_CUDA_CHECK(cudaMalloc(&base_, cap_));
+    free_[0] = cap_;
+    return TV_OK;
+  }
+  int64_t capacity() const { return cap_; }
+  // Blocks until `bytes` (≤ capacity) are free; returns offset.
+  int alloc(int64_t bytes, int64_t* off, ErrorSlot& err) {
+    bytes = (bytes + 255) & ~int64_t(255);
+    if (bytes > cap_) {
+      set_error("staging request " + std::to_string(bytes) + " > capacity " +
+                std::to_string(cap_));
+      return TV_ERR_NOMEM;
+    }
+    std::unique_lock<std::mutex> g(m_);
+    for (;;) {
+      reap(false);
+      for (auto it = free_.begin(); it != free_.end(); ++it) {
+        if (it->second >= bytes) {
+          *off = it->first;
+          int64_t rest = it->second - bytes, at = it->first + bytes;
+          free_.erase(it);
+          if (rest) free_[at] = rest;
+          return TV_OK;
+        }
+      }
+      if (err.failed.load()) return TV_ERR_STATE;
+      if (pending_.empty()) {
+        g.unlock();
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+        g.lock();
+        continue;
+      }
+      reap(true);  // wait for the oldest pending free
+    }
+  }
+  // Free [off, off+bytes) once `ev` (recorded after the last reader) completes.
+  void free_after(int64_t off, int64_t bytes, cudaEvent_t ev) {
+    bytes = (bytes + 255) & ~int64_t(255);
+    std::lock_guard<std::mutex> g(m_);
+    pending_.push_back({off, bytes, ev});
+  }
+  char* base() const { return base_; }
+
+ private:
+  struct Pending {
+    int64_t off, len;
+    cudaEvent_t ev;
+  };
+  void release(int64_t off, int64_t len) {
+    auto it = free_.emplace(off, len).first;
+    auto next = std::next(it);
+    if (next != free_.end() && it->first + it->second == next->first) {
+      it->second += next->second;
+      free_.erase(next);
+    }
+    if (it != free_.begin()) {
+      auto prev = std::prev(it);
+      if (prev->first + prev->second == it->first) {
+        prev->second += it->second;
+        free_.erase(it);
+      }
+    }
+  }
+  void reap(bool block) {
+    while (!pending_.empty()) {
+      auto& p = pending_.front();
+      if (block) {
+        cudaEventSynchronize(p.ev);
+        block = false;
+      } else if (cudaEventQuery(p.ev) != cudaSuccess) {
+        break;
+      }
+      cudaEventDestroy(p.ev);
+      release(p.off, p.len);
+      pending_.pop_front();
+    }
+  }
+  int device_;
+  int64_t cap_;
+  char* base_ = nullptr;
+  std::mutex m_;
+  std::map<int64_t, int64_t> free_;
+  std::deque<Pending> pending_;
+};
+
+struct DeviceCtx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<JobUploader> uploader;
+  std::unique_ptr<StagingPool> staging;
+};
+
+}  // namespace
+}  // namespace tv
+
+struct tv_engine {
+  int n_slots;
+  int64_t slot_bytes;
+  int64_t staging_bytes;
+  int n_threads;
+  std::vector<char*> slots;  // pinned
+  std::mutex dev_m;
+  std::map<int, std::unique_ptr<tv::DeviceCtx>> devices;
+  std::mutex call_m;  // one save/load at a time per engine
+};
+
+namespace tv {
+namespace {
+
+int device_ctx(tv_engine* e, int device, DeviceCtx** out) {
+  std::lock_guard<std::mutex> g(e->dev_m);
+  auto it = e->devices.find(device);
+  if (it == e->devices.end()) {
+    auto ctx = std::make_unique<DeviceCtx>();
+    ctx->device = device;
+    TV_CUDA_CHECK(cudaSetDevice(device));
+    TV_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->uploader = std::make_unique<JobUploader>(device);
+    ctx->staging = std::make_unique<StagingPool>(device, e->staging_bytes);
+    int rc = ctx->staging->init();
+    if (rc != TV_OK) return rc;
+    it = e->devices.emplace(device, std::move(ctx)).first;
+  }
+  *out = it->second.get();
+  return TV_OK;
+}
+
+int64_t box_bytes(const int64_t* ext, int rank, int isz) {
+  int64_t n = isz;
+  for (int i = 0; i < rank; ++i) n *= ext[i];
+  return n;
+}
+
+// Split the box (origin `off`, extent `ext` inside an array) into consecutive sub-boxes
+// of at most max_bytes each, in row-major payload order.
+struct SubBox {
+  int64_t off[TV_MAX_RANK];
+  int64_t ext[TV_MAX_RANK];
+  int64_t nbytes;
+};
+void split_box(const int64_t* off, const int64_t* ext, int rank, int isz, int64_t max_bytes,
+               std::vector<SubBox>& out) {
+  SubBox b;
+  std::memcpy(b.off, off, sizeof(int64_t) * rank);
+  std::memcpy(b.ext, ext, sizeof(int64_t) * rank);
+  b.nbytes = box_bytes(ext, rank, isz);
+  if (b.nbytes <= max_bytes || rank == 0) {
+    out.push_back(b);
+    return;
+  }
+  int d = 0;
+  while (d < rank && ext[d] == 1) ++d;
+  const int64_t row = b.nbytes / ext[d];
+  if (row <= max_bytes) {
+    const int64_t per = std::max<int64_t>(1, max_bytes / row);
+    for (int64_t i = 0; i < ext[d]; i += per) {
+      SubBox s = b;
+      s.off[d] = off[d] + i;
+      s.ext[d] = std::min(per, ext[d] - i);
+      s.nbytes = row * s.ext[d];
+      out.push_back(s);
+    }
+    return;
+  }
+  for (int64_t i = 0; i < ext[d]; ++i) {
+    int64_t o2[TV_MAX_RANK], e2[TV_MAX_RANK];
+    std::memcpy(o2, off, sizeof(int64_t) * rank);
+    std::memcpy(e2, ext, sizeof(int64_t) * rank);
+    o2[d] = off[d] + i;
+    e2[d] = 1;
+    split_box(o2, e2, rank, isz, max_bytes, out);
+  }
+}
+
+// ---- save ------------------------------------------------------------------------------
+
+struct WriteSeg {     // bytes of one output inside one slot
+  int out;
+  int64_t slot_off;
+  int64_t file_off;
+  int64_t n;
+};
+struct D2HSeg {       // contiguous device range → slot
+  const char* src;
+  int64_t slot_off;
+  int64_t n;
+};
+struct SaveSlot {
+  int index = -1;
+  int device = -1;
+  int64_t fill = 0;
+  std::vector<WriteSeg> writes;
+  std::vector<D2HSeg> d2h;
+  std::vector<tv_copy> packs;        // dst = staging
+  std::vector<int64_t> pack_offs;    // slot offset of each pack
+  cudaEvent_t ev = nullptr;
+};
+
+struct OutputState {
+  std::string path;   // empty → host buffer
+  char* host = nullptr;
+  int64_t size = 0;
+  std::atomic<int64_t> left{0};
+  std::once_flag opened;
+  int fd = -1;
+  std::atomic<bool> committed{false};
+};
+
+class SaveRun {
+ public:
+  SaveRun(tv_engine* e, const tv_write_item* items, int n_items, const tv_output* outs,
+          int n_outs, tv_stats* st)
+      : e_(e), items_(items), n_items_(n_items), n_outs_(n_outs), stats_(st) {
+    outs_.reset(new OutputState[n_outs]);
+    for (int i = 0; i < n_outs; ++i) {
+      outs_[i].path = outs[i].path ? outs[i].path : "";
+      outs_[i].host = reinterpret_cast<char*>(outs[i].host);
+      outs_[i].size = outs[i].size;
+      outs_[i].left.store(outs[i].size);
+    }
+  }
+
+  int run() {
+    const double t0 = now_s();
+    // Validate coverage: every output byte must be produced exactly by the items.
+    std::vector<int64_t> produced(n_outs_, 0);
+    for (int i = 0; i < n_items_; ++i) {
+      const auto& it = items_[i];
+      if (it.file < 0 || it.file >= n_outs_ || it.rank < 0 || it.rank > TV_MAX_RANK ||
+          it.itemsize <= 0) {
+        set_error("malformed write item " + std::to_string(i));
+        return TV_ERR_ARG;
+      }
+      int64_t n = box_bytes(it.ext, it.rank, it.itemsize);
+      if (it.file_off < 0 || it.file_off + n > outs_[it.file].size) {
+        set_error("write item " + std::to_string(i) + " outside its output");
+        return TV_ERR_ARG;
+      }
+      produced[it.file] += n;
+    }
+    for (int o = 0; o < n_outs_; ++o) {
+      if (produced[o] != outs_[o].size) {
+        set_error("output " + std::to_string(o) + " covered by " + std::to_string(produced[o]) +
+                  " of " + std::to_string(outs_[o].size) + " bytes");
+        return TV_ERR_ARG;
+      }
+    }
+    for (int s = 0; s < e_->n_slots; ++s) free_slots_.push(s);
+    std::vector<std::thread> writers;
+    for (int t = 0; t < e_->n_threads; ++t) writers.emplace_back([this] { writer_loop(); });
+    // Zero-byte outputs are committed up front.
+    for (int o = 0; o < n_outs_; ++o)
+      if (outs_[o].size == 0) finish_output(o);
+    produce();
+    ready_.close();
+    for (auto& w : writers) w.join();
+    for (auto& ev : events_) cudaEventDestroy(ev);
+    if (err_.failed.load()) {
+      abort_outputs();
+      set_error(err_.msg);
+      return err_.code;
+    }
+    stats_->seconds_total += now_s() - t0;
+    return TV_OK;
+  }
+
+ private:
+  void produce() {
+    SaveSlot cur;
+    auto flush = [&]() -> bool {
+      if (cur.index < 0) return true;
+      if (!submit(cur)) return false;
+      cur = SaveSlot();
+      return true;
+    };
+    auto open_slot = [&](int device) -> bool {
+      int s;
+      if (!free_slots_.pop(s)) return false;
+      cur.index = s;
+      cur.device = device;
+      cur.fill = 0;
+      return true;
+    };
+    const int64_t cap = e_->slot_bytes;
+    const size_t max_packs = 512;
+    for (int i = 0; i < n_items_ && !err_.failed.load(); ++i) {
+      const auto& it = items_[i];
+      const int64_t n = box_bytes(it.ext, it.rank, it.itemsize);
+      if (n == 0) continue;
+      int64_t boff = 0, bn = 0;
+      const bool contig = box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn);
+      if (contig) {
+        const char* src = reinterpret_cast<const char*>(it.src.base) + boff;
+        int64_t done = 0;
+        while (done < n) {
+          if (cur.index >= 0 && (cur.device != it.device || cur.fill == cap)) {
+            if (!flush()) return;
+          }
+          if (cur.index < 0 && !open_slot(it.device)) return;
+          const int64_t take = std::min(n - done, cap - cur.fill);
+          cur.d2h.push_back({src + done, cur.fill, take});
+          cur.writes.push_back({it.file, cur.fill, it.file_off + done, take});
+          cur.fill += take;
+          done += take;
+        }
+      } else {
+        std::vector<SubBox> subs;
+        split_box(it.src.off, it.ext, it.rank, it.itemsize, cap, subs);
+        int64_t payload = 0;
+        for (auto& sb : subs) {
+          if (cur.index >= 0 && (cur.device != it.device || cur.fill + sb.nbytes > cap ||
+                                 cur.packs.size() >= max_packs)) {
+            if (!flush()) return;
+          }
+          if (cur.index < 0 && !open_slot(it.device)) return;
+          tv_copy c{};
+          c.src = it.src;
+          std::memcpy(c.src.off, sb.off, sizeof(int64_t) * it.rank);
+          std::memcpy(c.ext, sb.ext, sizeof(int64_t) * it.rank);
+          c.rank = it.rank;
+          c.itemsize = it.itemsize;
+          // dst filled in submit() once the staging address is known
+          for (int d = 0; d < it.rank; ++d) {
+            c.dst.shape[d] = sb.ext[d];
+            c.dst.off[d] = 0;
+          }
+          cur.packs.push_back(c);
+          cur.pack_offs.push_back(cur.fill);
+          cur.writes.push_back({it.file, cur.fill, it.file_off + payload, sb.nbytes});
+          cur.fill += sb.nbytes;
+          payload += sb.nbytes;
+        }
+      }
+    }
+    flush();
+  }
+
+  bool submit(SaveSlot& s) {
+    DeviceCtx* ctx = nullptr;
+    int rc = device_ctx(e_, s.device, &ctx);
+    if (rc != TV_OK) {
+      err_.set(rc, get_error());
+      return false;
+    }
+    if (cudaSetDevice(s.device) != cudaSuccess) {
+      err_.set(TV_ERR_CUDA, "cudaSetDevice failed");
+      return false;
+    }
+    char* host = e_->slots[s.index];
+    if (!s.packs.empty()) {
+      if (ctx->staging->capacity() < (int64_t)e_->n_slots * e_->slot_bytes) {
+        err_.set(TV_ERR_NOMEM, "device staging smaller than n_slots*slot_bytes");
+        return false;
+      }
+      char* stage = ctx->staging->base() + (int64_t)s.index * e_->slot_bytes;
+      std::vector<CopyJob> jobs;
+      std::string why;
+      for (size_t k = 0; k < s.packs.size(); ++k) {
+        s.packs[k].dst.base = reinterpret_cast<uint64_t>(stage + s.pack_offs[k]);
+        if (!normalize(s.packs[k], jobs, why)) {
+          err_.set(TV_ERR_ARG, "pack: " + why);
+          return false;
+        }
+        stats_bytes_packed_ += box_bytes(s.packs[k].ext, s.packs[k].rank, s.packs[k].itemsize);
+      }
+      int64_t launches = 0;
+      rc = ctx->uploader->run(jobs, ctx->stream, &launches);
+      if (rc != TV_OK) {
+        err_.set(rc, get_error());
+        return false;
+      }
+      stats_launches_ += launches;
+      // D2H the packed bytes (adjacent packs coalesced).
+      for (size_t k = 0; k < s.packs.size();) {
+        int64_t start = s.pack_offs[k];
+        int64_t end = start + box_bytes(s.packs[k].ext, s.packs[k].rank, s.packs[k].itemsize);
+        size_t j = k + 1;
+        while (j < s.packs.size() && s.pack_offs[j] == end) {
+          end += box_bytes(s.packs[j].ext, s.packs[j].rank, s.packs[j].itemsize);
+          ++j;
+        }
+        s.d2h.push_back({stage + start, start, end - start});
+        k = j;
+      }
+    }
+    for (auto& d : s.d2h) {
+      if (cudaMemcpyAsync(host + d.slot_off, d.src, d.n, cudaMemcpyDeviceToHost, ctx->stream) !=
+          cudaSuccess) {
+        err_.set(TV_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(cudaGetLastError()));
+        return false;
+      }
+      stats_dma_ += 1;
+      stats_bytes_device_ += d.n;
+    }
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ev, ctx->stream) != cudaSuccess) {
+      err_.set(TV_ERR_CUDA, "event record failed");
+      return false;
+    }
+    {
+      std::lock_guard<std::mutex> g(ev_m_);
+      events_.push_back(ev);
+    }
+    s.ev = ev;
+    ready_.push(std::move(s));
+    return true;
+  }
+
+  void writer_loop() {
+    SaveSlot s;
+    while (ready_.pop(s)) {
+      if (!err_.failed.load()) {
+        cudaError_t ce = cudaEventSynchronize(s.ev);
+        if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("D2H/pack: ") + cudaGetErrorString(ce));
+      }
+      if (!err_.failed.load()) {
+        const char* host = e_->slots[s.index];
+        for (auto& w : s.writes) {
+          if (!write_seg(w, host)) break;
+        }
+      }
+      free_slots_.push(s.index);
+    }
+  }
+
+  bool write_seg(const WriteSeg& w, const char* host) {
+    OutputState& o = outs_[w.out];
+    if (o.path.empty()) {
+      std::memcpy(o.host + w.file_off, host + w.slot_off, w.n);
+    } else {
+      std::call_once(o.opened, [&] {
+        std::string err;
+        if (!dirs_.ensure(parent_of(o.path), err)) {
+          err_.set(TV_ERR_IO, err);
+          return;
+        }
+        std::string tmp = o.path + ".partial";
+        o.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0666);
+        if (o.fd < 0) err_.set(TV_ERR_IO, errno_msg("open", tmp));
+      });
+      if (o.fd < 0) return false;
+      int64_t done = 0;
+      while (done < w.n) {
+        ssize_t r = ::pwrite(o.fd, host + w.slot_off + done, w.n - done, w.file_off + done);
+        if (r < 0) {
+          if (errno == EINTR) continue;
+          err_.set(TV_ERR_IO, errno_msg("pwrite", o.path));
+          return false;
+        }
+        done += r;
+      }
+    }
+    stats_bytes_storage_ += w.n;
+    if (o.left.fetch_sub(w.n) == w.n) return finish_output(w.out);
+    return true;
+  }
+
+  bool finish_output(int idx) {
+    OutputState& o = outs_[idx];
+    if (o.path.empty()) {
+      o.committed.store(true);
+      return true;
+    }
+    if (o.size == 0) {
+      std::call_once(o.opened, [&] {
+        std::string err;
+        if (!dirs_.ensure(parent_of(o.path), err)) {
+          err_.set(TV_ERR_IO, err);
+          return;
+        }
+        std::string tmp = o.path + ".partial";
+        o.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0666);
+        if (o.fd < 0) err_.set(TV_ERR_IO, errno_msg("open", tmp));
+      });
+      if (o.fd < 0) return false;
+    }
+    if (::close(o.fd) != 0) {
+      err_.set(TV_ERR_IO, errno_msg("close", o.path));
+      return false;
+    }
+    o.fd = -1;
+    std::string tmp = o.path + ".partial";
+    if (::rename(tmp.c_str(), o.path.c_str()) != 0) {
+      err_.set(TV_ERR_IO, errno_msg("rename", tmp));
+      return false;
+    }
+    o.committed.store(true);
+    files_ += 1;
+    return true;
+  }
+
+  void abort_outputs() {
+    for (int i = 0; i < n_outs_; ++i) {
+      OutputState& o = outs_[i];
+      if (o.path.empty() || o.committed.load()) continue;
+      if (o.fd >= 0) {
+        ::close(o.fd);
+        o.fd = -1;
+        ::unlink((o.path + ".partial").c_str());
+      }
+    }
+  }
+
+ public:
+  void publish_stats() {
+    stats_->bytes_device += stats_bytes_device_.load();
+    stats_->bytes_storage += stats_bytes_storage_.load();
+    stats_->bytes_packed += stats_bytes_packed_.load();
+    stats_->kernel_launches += stats_launches_.load();
+    stats_->dma_copies += stats_dma_.load();
+    stats_->files += files_.load();
+  }
+
+ private:
+  tv_engine* e_;
+  const tv_write_item* items_;
+  int n_items_;
+  int n_outs_;
+  tv_stats* stats_;
+  std::unique_ptr<OutputState[]> outs_;
+  Queue<int> free_slots_;
+  Queue<SaveSlot> ready_;
+  ErrorSlot err_;
+  DirMaker dirs_;
+  std::mutex ev_m_;
+  std::vector<cudaEvent_t> events_;
+  std::atomic<int64_t> stats_bytes_device_{0}, stats_bytes_storage_{0}, stats_bytes_packed_{0},
+      stats_launches_{0}, stats_dma_{0}, files_{0};
+};
+
+// ---- restore -----------------------------------------------------------------------------
+
+struct InputState {
+  std::string path;
+  const char* host = nullptr;
+  int64_t size = 0;
+  std::once_flag opened;
+  int fd = -1;
+};
+
+struct ItemState {
+  std::atomic<int> left{0};
+  char* base = nullptr;      // landing address on the reader device
+  int64_t staged_off = -1;   // staging offset when not direct
+};
+
+struct ReadTask {
+  int item;
+  int slot;
+  int64_t off;   // within the item
+  int64_t n;
+};
+
+class LoadRun {
+ public:
+  LoadRun(tv_engine* e, const tv_read_item* items, int n_items, const tv_input* ins, int n_ins,
+          const tv_copy* copies, int n_copies, tv_stats* st)
+      : e_(e), items_(items), n_items_(n_items), n_ins_(n_ins), copies_(copies),
+        n_copies_(n_copies), stats_(st) {
+    ins_.reset(new InputState[n_ins]);
+    for (int i = 0; i < n_ins; ++i) {
+      ins_[i].path = ins[i].path ? ins[i].path : "";
+      ins_[i].host = reinterpret_cast<const char*>(ins[i].host);
+      ins_[i].size = ins[i].size;
+    }
+    states_.reset(new ItemState[n_items > 0 ? n_items : 1]);
+    slot_events_.assign(e->n_slots, nullptr);
+    slot_event_dev_.assign(e->n_slots, -1);
+  }
+
+  int run() {
+    const double t0 = now_s();
+    for (int i = 0; i < n_items_; ++i) {
+      const auto& it = items_[i];
+      if (it.input < 0 || it.input >= n_ins_ || it.nbytes < 0 || it.first_copy < 0 ||
+          it.n_copies < 0 || it.first_copy + it.n_copies > n_copies_) {
+        set_error("malformed read item " + std::to_string(i));
+        return TV_ERR_ARG;
+      }
+      if (ins_[it.input].size >= 0 && it.in_off + it.nbytes > ins_[it.input].size) {
+        set_error("read item " + std::to_string(i) + " beyond the end of its input");
+        return TV_ERR_ARG;
+      }
+      if (it.direct_dst == 0 && it.n_copies == 0) {
+        set_error("read item " + std::to_string(i) + " has no destination");
+        return TV_ERR_ARG;
+      }
+    }
+    for (int s = 0; s < e_->n_slots; ++s) free_slots_.push(s);
+    std::vector<std::thread> readers;
+    for (int t = 0; t < e_->n_threads; ++t) readers.emplace_back([this] { reader_loop(); });
+    produce();
+    tasks_.close();
+    for (auto& r : readers) r.join();
+    // Drain all devices used.
+    for (auto& kv : used_devices_) {
+      cudaSetDevice(kv.first);
+      cudaError_t ce = cudaStreamSynchronize(kv.second->stream);
+      if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("restore stream: ") + cudaGetErrorString(ce));
+    }
+    for (int s = 0; s < e_->n_slots; ++s)
+      if (slot_events_[s]) cudaEventDestroy(slot_events_[s]);
+    for (int i = 0; i < n_ins_; ++i)
+      if (ins_[i].fd >= 0) ::close(ins_[i].fd);
+    if (err_.failed.load()) {
+      set_error(err_.msg);
+      return err_.code;
+    }
+    stats_->seconds_total += now_s() - t0;
+    return TV_OK;
+  }
+
+  void publish_stats() {
+    stats_->bytes_device += bytes_device_.load();
+    stats_->bytes_storage += bytes_storage_.load();
+    stats_->bytes_packed += bytes_packed_.load();
+    stats_->kernel_launches += launches_.load();
+    stats_->dma_copies += dma_.load();
+    stats_->files += files_.load();
+  }
+
+ private:
+  DeviceCtx* ctx_for(int device) {
+    std::lock_guard<std::mutex> g(used_m_);
+    auto it = used_devices_.find(device);
+    if (it != used_devices_.end()) return it->second;
+    DeviceCtx* ctx = nullptr;
+    int rc = device_ctx(e_, device, &ctx);
+    if (rc != TV_OK) {
+      err_.set(rc, get_error());
+      return nullptr;
+    }
+    used_devices_[device] = ctx;
+    return ctx;
+  }
+
+  int acquire_slot() {
+    int s;
+    if (!free_slots_.pop(s)) return -1;
+    if (slot_events_[s]) {
+      cudaSetDevice(slot_event_dev_[s]);
+      cudaEventSynchronize(slot_events_[s]);  // previous H2D out of this slot done
+    }
+    return s;
+  }
+
+  void produce() {
+    const int64_t cap = e_->slot_bytes;
+    for (int i = 0; i < n_items_ && !err_.failed.load(); ++i) {
+      const auto& it = items_[i];
+      if (it.nbytes == 0) continue;  // nothing to land, nothing to scatter
+      DeviceCtx* ctx = ctx_for(it.device);
+      if (!ctx) return;
+      ItemState& st = states_[i];
+      if (it.direct_dst) {
+        st.base = reinterpret_cast<char*>(it.direct_dst);
+      } else {
+        int64_t off = 0;
+        int rc = ctx->staging->alloc(it.nbytes, &off, err_);
+        if (rc != TV_OK) {
+          err_.set(rc, get_error());
+          return;
+        }
+        st.staged_off = off;
+        st.base = ctx->staging->base() + off;
+      }
+      const int pieces = (int)((it.nbytes + cap - 1) / cap);
+      st.left.store(pieces);
+      for (int p = 0; p < pieces; ++p) {
+        int s = acquire_slot();
+        if (s < 0 || err_.failed.load()) return;
+        const int64_t off = (int64_t)p * cap;
+        tasks_.push({i, s, off, std::min(cap, it.nbytes - off)});
+      }
+    }
+  }
+
+  void reader_loop() {
+    ReadTask t;
+    while (tasks_.pop(t)) {
+      bool released = false;
+      if (!err_.failed.load()) released = run_task(t);
+      if (!released) free_slots_.push(t.slot);
+    }
+  }
+
+  bool fetch(InputState& in, char* dst, int64_t off, int64_t n) {
+    if (in.path.empty()) {
+      std::memcpy(dst, in.host + off, n);
+      return true;
+    }
+    std::call_once(in.opened, [&] {
+      in.fd = ::open(in.path.c_str(), O_RDONLY | O_CLOEXEC);
+      if (in.fd < 0) err_.set(TV_ERR_IO, errno_msg("open", in.path));
+      else files_ += 1;
+    });
+    if (in.fd < 0) return false;
+    int64_t done = 0;
+    while (done < n) {
+      ssize_t r = ::pread(in.fd, dst + done, n - done, off + done);
+      if (r < 0) {
+        if (errno == EINTR) continue;
+        err_.set(TV_ERR_IO, errno_msg("pread", in.path));
+        return false;
+      }
+      if (r == 0) {
+        err_.set(TV_ERR_IO, "short read from " + in.path);
+        return false;
+      }
+      done += r;
+    }
+    return true;
+  }
+
+  // Returns true when the slot has been handed back to the free list.
+  bool run_task(const ReadTask& t) {
+    const auto& it = items_[t.item];
+    ItemState& st = states_[t.item];
+    char* host = e_->slots[t.slot];
+    if (!fetch(ins_[it.input], host, it.in_off + t.off, t.n)) return false;
+    bytes_storage_ += t.n;
+    DeviceCtx* ctx = ctx_for(it.device);
+    if (!ctx) return false;
+    cudaSetDevice(it.device);
+    if (cudaMemcpyAsync(st.base + t.off, host, t.n, cudaMemcpyHostToDevice, ctx->stream) !=
+        cudaSuccess) {
+      err_.set(TV_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(cudaGetLastError()));
+      return false;
+    }
+    dma_ += 1;
+    bytes_device_ += t.n;
+    cudaEvent_t& ev = slot_events_[t.slot];
+    if (ev && slot_event_dev_[t.slot] != it.device) {
+      cudaEventDestroy(ev);
+      ev = nullptr;
+    }
+    if (!ev) {
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      slot_event_dev_[t.slot] = it.device;
+    }
+    cudaEventRecord(ev, ctx->stream);
+    free_slots_.push(t.slot);
+    if (st.left.fetch_sub(1) == 1) launch_copies(t.item);
+    return true;
+  }
+
+  void launch_copies(int item) {
+    const auto& it = items_[item];
+    ItemState& st = states_[item];
+    DeviceCtx* ctx = ctx_for(it.device);
+    if (!ctx) return;
+    cudaSetDevice(it.device);
+    if (it.n_copies > 0) {
+      std::vector<CopyJob> jobs;
+      std::string why;
+      for (int c = 0; c < it.n_copies; ++c) {
+        tv_copy cp = copies_[it.first_copy + c];
+        cp.src.base = reinterpret_cast<uint64_t>(st.base) + cp.src.base;
+        if (!normalize(cp, jobs, why)) {
+          err_.set(TV_ERR_ARG, "unpack: " + why);
+          return;
+        }
+        bytes_packed_ += box_bytes(cp.ext, cp.rank, cp.itemsize);
+      }
+      int64_t launches = 0;
+      int rc = ctx->uploader->run(jobs, ctx->stream, &launches);
+      if (rc != TV_OK) {
+        err_.set(rc, get_error());
+        return;
+      }
+      launches_ += launches;
+    }
+    if (st.staged_off >= 0) {
+      cudaEvent_t ev;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      cudaEventRecord(ev, ctx->stream);
+      ctx->staging->free_after(st.staged_off, it.nbytes, ev);
+    }
+  }
+
+  tv_engine* e_;
+  const tv_read_item* items_;
+  int n_items_;
+  int n_ins_;
+  const tv_copy* copies_;
+  int n_copies_;
+  tv_stats* stats_;
+  std::unique_ptr<InputState[]> ins_;
+  std::unique_ptr<ItemState[]> states_;
+  std::vector<cudaEvent_t> slot_events_;
+  std::vector<int> slot_event_dev_;
+  Queue<int> free_slots_;
+  Queue<ReadTask> tasks_;
+  ErrorSlot err_;
+  std::mutex used_m_;
+  std::map<int, DeviceCtx*> used_devices_;
+  std::atomic<int64_t> bytes_device_{0}, bytes_storage_{0}, bytes_packed_{0}, launches_{0},
+      dma_{0}, files_{0};
+};
+
+}  // namespace
+
+int engine_create(int n_slots, int64_t slot_bytes, int64_t staging_bytes, int n_threads,
+                  tv_engine** out) {
+  if (n_slots < 1 || slot_bytes < 4096 || n_threads < 1 || staging_bytes < 0) {
+    set_error("bad engine parameters");
+    return TV_ERR_ARG;
+  }
+  auto e = std::make_unique<tv_engine>();
+  e->n_slots = n_slots;
+  e->slot_bytes = slot_bytes;
+  e->staging_bytes = std::max<int64_t>(staging_bytes, (int64_t)n_slots * slot_bytes);
+  e->n_threads = n_threads;
+  for (int i = 0; i < n_slots; ++i) {
+    char* p = nullptr;
+    cudaError_t ce = cudaHostAlloc(&p, slot_bytes, cudaHostAllocPortable);
+    if (ce != cudaSuccess) {
+      for (auto q : e->slots) cudaFreeHost(q);
+      set_error(std::string("cudaHostAlloc: ") + cudaGetErrorString(ce));
+      return TV_ERR_NOMEM;
+    }
+    e->slots.push_back(p);
+  }
+  *out = e.release();
+  return TV_OK;
+}
+
+int engine_destroy(tv_engine* e) {
+  if (!e) return TV_OK;
+  {
+    std::lock_guard<std::mutex> g(e->dev_m);
+    for (auto& kv : e->devices) {
+      cudaSetDevice(kv.first);
+      cudaStreamSynchronize(kv.second->stream);
+      kv.second->uploader.reset();
+      kv.second->staging.reset();
+      cudaStreamDestroy(kv.second->stream);
+    }
+    e->devices.clear();
+  }
+  for (auto p : e->slots) cudaFreeHost(p);
+  delete e;
+  return TV_OK;
+}
+
+int engine_save(tv_engine* e, const tv_write_item* items, int n_items, const tv_output* outputs,
+                int n_outputs, tv_stats* stats) {
+  std::lock_guard<std::mutex> g(e->call_m);
+  tv_stats local{};
+  SaveRun run(e, items, n_items, outputs, n_outputs, stats ? stats : &local);
+  int rc = run.run();
+  run.publish_stats();
+  return rc;
+}
+
+int engine_load(tv_engine* e, const tv_read_item* items, int n_items, const tv_input* inputs,
+                int n_inputs, const tv_copy* copies, int n_copies, tv_stats* stats) {
+  std::lock_guard<std::mutex> g(e->call_m);
+  tv_stats local{};
+  LoadRun run(e, items, n_items, inputs, n_inputs, copies, n_copies, stats ? stats : &local);
+  int rc = run.run();
+  run.publish_stats();
+  return rc;
+}
+
+// Standalone batched copy (tv_copy_boxes): one launch on the caller's stream.
+int copy_boxes(int device, const tv_copy* copies, int n, cudaStream_t stream) {
+  std::vector<CopyJob> jobs;
+  std::string why;
+  for (int i = 0; i < n; ++i) {
+    if (!normalize(copies[i], jobs, why)) {
+      set_error("tv_copy_boxes: copy " + std::to_string(i) + ": " + why);
+      return TV_ERR_ARG;
+    }
+  }
+  if (jobs.empty()) return TV_OK;
+  static std::mutex m;
+  static std::map<int, std::unique_ptr<JobUploader>> uploaders;
+  JobUploader* up;
+  {
+    std::lock_guard<std::mutex> g(m);
+    auto& slot = uploaders[device];
+    if (!slot) slot = std::make_unique<JobUploader>(device);
+    up = slot.get();
+  }
+  TV_CUDA_CHECK(cudaSetDevice(device));
+  return up->run(jobs, stream, nullptr);
+}
+
+}  // namespace tv

@@ -1,0 +1,58 @@
+// Internal declarations shared by the libtvgpu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tvgpu.h"
+
+namespace tv {
+
+// Thread-local last error (tv_last_error).
+void set_error(const std::string& msg);
+const std::string& get_error();
+
+#define TV_CUDA_CHECK(expr)                                                              \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess) {                                                             \
+      ::tv::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" +        \
+                      __FILE__ + ":" + std::to_string(__LINE__) + ")");                  \
+      return TV_ERR_CUDA;                                                                \
+    }                                                                                    \
+  } while (0)
+
+// Canonical form of one box copy: `nruns` contiguous runs of `run` bytes, the run
+// index decomposed over up to three outer dimensions (n[0] fastest) with byte strides
+// ss/ds on the source/destination side.  Produced on the host by normalize().
+struct CopyJob {
+  const char* src;
+  char* dst;
+  int64_t run;        // bytes per contiguous run (identical on both sides)
+  int64_t n[3];       // outer extents (n[0] varies fastest); unused dims are 1
+  int64_t ss[3];      // source byte strides of the outer dims
+  int64_t ds[3];      // destination byte strides
+  int64_t nruns;      // n[0]*n[1]*n[2]
+  int64_t units;      // work units of this job (see kernel)
+  int64_t unit_begin; // prefix sum of units over the batch
+  int32_t vec;        // vector width in bytes (1,2,4,8,16)
+  int32_t mode;       // 0 = warp per run segment, 1 = flat (short runs)
+};
+
+// Split a tv_copy into canonical jobs (appends; returns false on malformed input).
+bool normalize(const tv_copy& c, std::vector<CopyJob>& out, std::string& err);
+
+// Assign units/unit_begin and launch the batched copy kernel on `stream`.
+// `dev_jobs` must point to device-visible memory holding `jobs` (the caller stages it).
+int64_t plan_units(std::vector<CopyJob>& jobs);
+cudaError_t launch_copy_jobs(const CopyJob* dev_jobs, int n_jobs, int64_t total_units,
+                             cudaStream_t stream);
+
+// Is the box a single contiguous byte range of its array?  Sets byte offset/length.
+bool box_contiguous(const tv_array_box& b, const int64_t* ext, int rank, int itemsize,
+                    int64_t* byte_off, int64_t* nbytes);
+
+}  // namespace tv

@@ -1,0 +1,299 @@
+"""ctypes binding of libtvgpu.so (include/tvgpu.h) and the engine pool.
+
+The library is built in-tree by ``paper_2605_23066_b200.build`` (``__graft_entry__.build``)
+and loaded from the package directory.  There is no fallback: if the library is missing
+or no GPU is visible, every data-path entry point raises ``NativeError``.
+
+Descriptor tables cross the boundary as numpy structured arrays whose layout equals the
+C structs (checked against a compiled ``offsetof`` probe in tests/test_native_abi.py), so
+a save of thousands of chunks builds its tables with vectorised column writes instead of
+one ctypes object per chunk.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+
+from .errors import NativeError
+
+MAX_RANK = 8
+LIB_PATH = Path(__file__).resolve().parent / "libtvgpu.so"
+
+TV_OK = 0
+
+# ---- C struct layouts -------------------------------------------------------------------
+
+ARRAY_BOX = np.dtype(
+    [("base", "<u8"), ("shape", "<i8", (MAX_RANK,)), ("off", "<i8", (MAX_RANK,))], align=True
+)
+COPY = np.dtype(
+    [("src", ARRAY_BOX), ("dst", ARRAY_BOX), ("ext", "<i8", (MAX_RANK,)), ("rank", "<i4"),
+     ("itemsize", "<i4")],
+    align=True,
+)
+WRITE_ITEM = np.dtype(
+    [("src", ARRAY_BOX), ("ext", "<i8", (MAX_RANK,)), ("rank", "<i4"), ("itemsize", "<i4"),
+     ("file", "<i4"), ("device", "<i4"), ("file_off", "<i8")],
+    align=True,
+)
+OUTPUT = np.dtype([("path", "<u8"), ("host", "<u8"), ("size", "<i8")], align=True)
+READ_ITEM = np.dtype(
+    [("input", "<i4"), ("device", "<i4"), ("in_off", "<i8"), ("nbytes", "<i8"),
+     ("direct_dst", "<u8"), ("first_copy", "<i4"), ("n_copies", "<i4")],
+    align=True,
+)
+INPUT = OUTPUT
+STATS = np.dtype(
+    [("bytes_device", "<i8"), ("bytes_storage", "<i8"), ("bytes_packed", "<i8"),
+     ("kernel_launches", "<i8"), ("dma_copies", "<i8"), ("files", "<i8"),
+     ("seconds_total", "<f8"), ("seconds_kernel", "<f8")],
+    align=True,
+)
+
+# Every symbol include/tvgpu.h declares (tests check the library exports all of them).
+EXPORTS = (
+    "tv_abi_version", "tv_last_error", "tv_copy_boxes", "tv_copy_bytes", "tv_engine_create",
+    "tv_engine_destroy", "tv_engine_save", "tv_engine_load", "tv_enable_peer_access",
+    "tv_ipc_export", "tv_ipc_import", "tv_ipc_close", "tv_probe_storage", "tv_probe_pcie",
+)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _declare(lib: ctypes.CDLL) -> None:
+    P, I, L, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "tv_abi_version": (I, []),
+        "tv_last_error": (I, [ctypes.c_char_p, ctypes.c_size_t]),
+        "tv_copy_boxes": (I, [I, P, I, P]),
+        "tv_copy_bytes": (L, [P, I]),
+        "tv_engine_create": (I, [I, L, L, I, ctypes.POINTER(P)]),
+        "tv_engine_destroy": (I, [P]),
+        "tv_engine_save": (I, [P, P, I, P, I, P]),
+        "tv_engine_load": (I, [P, P, I, P, I, P, I, P]),
+        "tv_enable_peer_access": (I, [P, I]),
+        "tv_ipc_export": (I, [I, ctypes.c_uint64, P, ctypes.POINTER(ctypes.c_uint64)]),
+        "tv_ipc_import": (I, [I, P, ctypes.POINTER(ctypes.c_uint64)]),
+        "tv_ipc_close": (I, [I, ctypes.c_uint64]),
+        "tv_probe_storage": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D)]),
+        "tv_probe_pcie": (I, [I, L, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library; raises NativeError when it is absent (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise NativeError(
+                    f"{LIB_PATH} is missing: build it with `python -m "
+                    "paper_2605_23066_b200.build` (there is no CPU fallback)"
+                )
+            try:
+                handle = ctypes.CDLL(str(LIB_PATH))
+            except OSError as exc:
+                raise NativeError(f"cannot load {LIB_PATH}: {exc}") from exc
+            _declare(handle)
+            if handle.tv_abi_version() != 1:
+                raise NativeError("libtvgpu ABI version mismatch")
+            _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(4096)
+    lib().tv_last_error(buf, len(buf))
+    return buf.value.decode("utf-8", "replace")
+
+
+def check(rc: int, what: str) -> None:
+    if rc != TV_OK:
+        raise NativeError(f"{what} failed (code {rc}): {last_error()}")
+
+
+def require_gpu() -> None:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device: the B200 data path has no CPU fallback")
+
+
+def _ptr(arr: np.ndarray) -> int:
+    return arr.ctypes.data if arr.size else 0
+
+
+# ---- kernels ----------------------------------------------------------------------------
+
+
+def copy_boxes(device: int, copies: np.ndarray, stream: int = 0) -> None:
+    """One batched box-copy launch on ``device``/``stream`` (COPY-dtype table)."""
+    copies = np.ascontiguousarray(copies, dtype=COPY)
+    if copies.size == 0:
+        return
+    check(lib().tv_copy_boxes(device, _ptr(copies), len(copies), stream), "tv_copy_boxes")
+
+
+def enable_peer_access(gpus: Sequence[int]) -> None:
+    gpus = sorted(set(int(g) for g in gpus))
+    if len(gpus) < 2:
+        return
+    arr = (ctypes.c_int * len(gpus))(*gpus)
+    check(lib().tv_enable_peer_access(arr, len(gpus)), "tv_enable_peer_access")
+
+
+def ipc_export(device: int, ptr: int) -> tuple[bytes, int]:
+    handle = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64()
+    check(lib().tv_ipc_export(device, ptr, handle, ctypes.byref(off)), "tv_ipc_export")
+    return handle.raw, off.value
+
+
+def ipc_import(device: int, handle: bytes) -> int:
+    out = ctypes.c_uint64()
+    buf = ctypes.create_string_buffer(handle, 64)
+    check(lib().tv_ipc_import(device, buf, ctypes.byref(out)), "tv_ipc_import")
+    return out.value
+
+
+def ipc_close(device: int, ptr: int) -> None:
+    check(lib().tv_ipc_close(device, ptr), "tv_ipc_close")
+
+
+def probe_storage(directory: str, threads: int, file_bytes: int, block_bytes: int) -> tuple[float, float]:
+    w, r = ctypes.c_double(), ctypes.c_double()
+    check(
+        lib().tv_probe_storage(directory.encode(), threads, file_bytes, block_bytes,
+                               ctypes.byref(w), ctypes.byref(r)),
+        "tv_probe_storage",
+    )
+    return w.value, r.value
+
+
+def probe_pcie(device: int, nbytes: int = 1 << 30, reps: int = 3) -> tuple[float, float]:
+    d2h, h2d = ctypes.c_double(), ctypes.c_double()
+    check(lib().tv_probe_pcie(device, nbytes, reps, ctypes.byref(d2h), ctypes.byref(h2d)),
+          "tv_probe_pcie")
+    return d2h.value, h2d.value
+
+
+# ---- engine --------------------------------------------------------------------------------
+
+
+class PathTable:
+    """NUL-terminated path strings kept alive for one engine call."""
+
+    def __init__(self, paths: Sequence[str | None]):
+        encoded = [(p.encode() + b"\0") if p else b"" for p in paths]
+        self._blob = ctypes.create_string_buffer(b"".join(encoded) or b"\0")
+        base = ctypes.addressof(self._blob)
+        offs = np.zeros(len(encoded), np.uint64)
+        pos = 0
+        for i, e in enumerate(encoded):
+            offs[i] = (base + pos) if e else 0
+            pos += len(e)
+        self.pointers = offs
+
+
+class Engine:
+    """One libtvgpu engine: pinned slot ring + storage threads (+ per-device staging)."""
+
+    def __init__(self, n_slots: int, slot_bytes: int, staging_bytes: int, threads: int):
+        self.config = (n_slots, slot_bytes, staging_bytes, threads)
+        handle = ctypes.c_void_p()
+        check(lib().tv_engine_create(n_slots, slot_bytes, staging_bytes, threads,
+                                     ctypes.byref(handle)), "tv_engine_create")
+        self._h = handle
+
+    def close(self) -> None:
+        if self._h:
+            lib().tv_engine_destroy(self._h)
+            self._h = None
+
+    def save(self, items: np.ndarray, outputs: np.ndarray) -> np.ndarray:
+        stats = np.zeros(1, STATS)
+        items = np.ascontiguousarray(items, WRITE_ITEM)
+        outputs = np.ascontiguousarray(outputs, OUTPUT)
+        rc = lib().tv_engine_save(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
+                                  stats.ctypes.data)
+        check(rc, "tv_engine_save")
+        return stats[0]
+
+    def load(self, items: np.ndarray, inputs: np.ndarray, copies: np.ndarray) -> np.ndarray:
+        stats = np.zeros(1, STATS)
+        items = np.ascontiguousarray(items, READ_ITEM)
+        inputs = np.ascontiguousarray(inputs, INPUT)
+        copies = np.ascontiguousarray(copies, COPY)
+        rc = lib().tv_engine_load(self._h, _ptr(items), len(items), _ptr(inputs), len(inputs),
+                                  _ptr(copies), len(copies), stats.ctypes.data)
+        check(rc, "tv_engine_load")
+        return stats[0]
+
+
+class EngineConfig:
+    """Pipeline sizing.  Defaults: 32 × 8 MiB pinned slots (DDIO/L3-friendly pwrite
+    blocks, deep enough to keep PCIe busy while 16 threads write), device staging of the
+    same size, threads = host cores shared by the engines running at once."""
+
+    def __init__(self, slot_bytes: int | None = None, n_slots: int | None = None,
+                 staging_bytes: int | None = None, threads: int | None = None):
+        env = os.environ
+        self.slot_bytes = int(slot_bytes or env.get("TVGPU_SLOT_BYTES", 8 << 20))
+        self.n_slots = int(n_slots or env.get("TVGPU_SLOTS", 32))
+        self.staging_bytes = int(staging_bytes or env.get("TVGPU_STAGING_BYTES", 0)) or max(
+            self.n_slots * self.slot_bytes, 1 << 30
+        )
+        self.threads = threads or (int(env["TVGPU_THREADS"]) if "TVGPU_THREADS" in env else None)
+
+    def threads_for(self, concurrent: int) -> int:
+        if self.threads:
+            return self.threads
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        return max(2, (cores or 8) // max(1, concurrent))
+
+
+_pool: dict[tuple, list[Engine]] = {}
+_pool_lock = threading.Lock()
+
+
+class engine_lease:
+    """Context manager borrowing an idle engine of the given sizing from the pool."""
+
+    def __init__(self, cfg: EngineConfig, concurrent: int):
+        self.key = (cfg.n_slots, cfg.slot_bytes, cfg.staging_bytes, cfg.threads_for(concurrent))
+        self.engine: Engine | None = None
+
+    def __enter__(self) -> Engine:
+        require_gpu()
+        with _pool_lock:
+            idle = _pool.setdefault(self.key, [])
+            self.engine = idle.pop() if idle else None
+        if self.engine is None:
+            self.engine = Engine(*self.key)
+        return self.engine
+
+    def __exit__(self, *exc) -> None:
+        with _pool_lock:
+            _pool.setdefault(self.key, []).append(self.engine)
+
+
+def release_pool() -> None:
+    """Destroy every pooled engine (frees pinned memory)."""
+    with _pool_lock:
+        for engines in _pool.values():
+            for e in engines:
+                e.close()
+        _pool.clear()
