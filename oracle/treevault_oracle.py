@@ -385,3 +385,63 @@ def save_to_directory(root: str, files: dict[str, bytes]) -> int:
         os.replace(dst + ".partial", dst)
         total += len(data)
     return total
+
+
+def _read_range(root: str, path: str, scoped: str, entry: dict, ranges) -> np.ndarray:
+    """chunkstore.py:507-593 for whole-chunk fetches of per-leaf files."""
+    w = tuple(entry["write_chunk"])
+    dt = {"f32": "<f4", "f64": "<f8", "i32": "<i4", "i64": "<i8", "u8": "|u1", "bool": "|b1",
+          "bf16": "<u2"}[entry["dtype"]]
+    out = np.empty(tuple(e for _, e in ranges), dt)
+    for coords in cells(ranges, w):
+        loc = entry["chunks"][ckey(coords)]
+        fname = os.path.join(root, *path.split("/"), f"process_{loc['p']}", *scoped.split("/"),
+                             f"c.{ckey(coords)}")
+        with open(fname, "rb") as f:
+            chunk = np.frombuffer(f.read(), dt).reshape(w)
+        cell = tuple((c * s, s) for c, s in zip(coords, w))
+        hit = [(max(a, b), min(a + e, b + s) - max(a, b)) for (a, e), (b, s) in zip(ranges, cell)]
+        src = tuple(slice(h - b, h - b + n) for (h, n), (b, _) in zip(hit, cell))
+        dst = tuple(slice(h - a, h - a + n) for (h, n), (a, _) in zip(hit, ranges))
+        out[dst] = chunk[src]
+    return out
+
+
+def restore_from_directory(root: str, path: str, processes: int) -> dict[str, np.ndarray]:
+    """load_pipeline.py:406-493 on a per-leaf checkpoint saved with its own topology:
+    each simulated process (one thread) reads its devices' shard ranges, then the global
+    arrays are assembled."""
+    import threading
+
+    with open(os.path.join(root, *path.split("/"), "merged_index.json"), "rb") as f:
+        arrays = json.loads(f.read())["arrays"]
+    pieces: list[list] = [[] for _ in range(processes)]
+
+    def work(p):
+        for scoped, entry in arrays.items():
+            sh = entry["sharding"]
+            if sh is None:
+                if p == 0:
+                    whole = tuple((0, g) for g in entry["global_shape"])
+                    pieces[p].append((scoped, whole, _read_range(root, path, scoped, entry, whole)))
+                continue
+            spec = Spec(Mesh([tuple(a) for a in sh["axes"]], processes), sh["spec"], sh["global_shape"])
+            seen = set()
+            for dev, ranges, _ in spec.shards():
+                if spec.mesh.proc[dev] == p and ranges not in seen:
+                    seen.add(ranges)
+                    pieces[p].append((scoped, ranges, _read_range(root, path, scoped, entry, ranges)))
+
+    threads = [threading.Thread(target=work, args=(p,)) for p in range(processes)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    out = {}
+    for scoped, entry in arrays.items():
+        dt = {"f32": "<f4", "bf16": "<u2"}.get(entry["dtype"], "<f8")
+        out[scoped] = np.empty(tuple(entry["global_shape"]), dt)
+    for plist in pieces:
+        for scoped, ranges, data in plist:
+            out[scoped][tuple(slice(o, o + e) for o, e in ranges)] = data
+    return out

@@ -420,6 +420,7 @@ struct D2HSeg {       // contiguous device range → slot
 };
 struct SaveSlot {
   int index = -1;
+  int lane = 0;
   int device = -1;
   int64_t fill = 0;
   std::vector<WriteSeg> writes;
@@ -479,13 +480,14 @@ class SaveRun {
       }
     }
     for (int s = 0; s < e_->n_slots; ++s) free_slots_.push(s);
+    assign_lanes();
     std::vector<std::thread> writers;
-    for (int t = 0; t < e_->n_threads; ++t) writers.emplace_back([this] { writer_loop(); });
+    for (int t = 0; t < (int)lanes_.size(); ++t) writers.emplace_back([this, t] { writer_loop(t); });
     // Zero-byte outputs are committed up front.
     for (int o = 0; o < n_outs_; ++o)
       if (outs_[o].size == 0) finish_output(o);
     produce();
-    ready_.close();
+    for (auto& q : lanes_) q->close();
     for (auto& w : writers) w.join();
     for (auto& ev : events_) cudaEventDestroy(ev);
     if (err_.failed.load()) {
@@ -498,74 +500,125 @@ class SaveRun {
   }
 
  private:
-  void produce() {
-    SaveSlot cur;
-    auto flush = [&]() -> bool {
-      if (cur.index < 0) return true;
-      if (!submit(cur)) return false;
-      cur = SaveSlot();
-      return true;
-    };
-    auto open_slot = [&](int device) -> bool {
-      int s;
-      if (!free_slots_.pop(s)) return false;
-      cur.index = s;
-      cur.device = device;
-      cur.fill = 0;
-      return true;
-    };
+  // Files are distributed over writer lanes (one per storage thread), largest first onto
+  // the least-loaded lane: a file is only ever written by its lane's thread, because
+  // tmpfs (and most local filesystems) serialise concurrent writes to one inode.  The
+  // producer fills slots round-robin across lanes so every lane streams concurrently.
+  struct LaneCursor {
+    std::vector<int> items;  // item indices of this lane's files, in item order
+    size_t pos = 0;
+    int64_t done = 0;        // payload bytes of items[pos] already placed
+    std::vector<SubBox> subs;
+    size_t sub_pos = 0;
+    bool split = false;
+    bool finished() const { return pos >= items.size(); }
+  };
+
+  void assign_lanes() {
+    const int L = std::max(1, e_->n_threads);
+    lanes_.clear();
+    for (int k = 0; k < L; ++k) lanes_.emplace_back(new Queue<SaveSlot>());
+    cursors_.assign(L, LaneCursor());
+    std::vector<int> order(n_outs_);
+    for (int o = 0; o < n_outs_; ++o) order[o] = o;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return outs_[a].size > outs_[b].size; });
+    std::vector<int64_t> load(L, 0);
+    lane_of_.assign(n_outs_, 0);
+    for (int o : order) {
+      int best = 0;
+      for (int k = 1; k < L; ++k)
+        if (load[k] < load[best]) best = k;
+      lane_of_[o] = best;
+      load[best] += std::max<int64_t>(outs_[o].size, 1);
+    }
+    for (int i = 0; i < n_items_; ++i) cursors_[lane_of_[items_[i].file]].items.push_back(i);
+  }
+
+  // Fill slot `cur` from lane `k`; returns false on error.
+  bool fill_slot(LaneCursor& c, SaveSlot& cur) {
     const int64_t cap = e_->slot_bytes;
     const size_t max_packs = 512;
-    for (int i = 0; i < n_items_ && !err_.failed.load(); ++i) {
-      const auto& it = items_[i];
+    while (!c.finished()) {
+      const auto& it = items_[c.items[c.pos]];
       const int64_t n = box_bytes(it.ext, it.rank, it.itemsize);
-      if (n == 0) continue;
+      if (n == 0) {
+        ++c.pos;
+        continue;
+      }
+      if (cur.device >= 0 && cur.device != it.device) return true;
       int64_t boff = 0, bn = 0;
-      const bool contig = box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn);
-      if (contig) {
-        const char* src = reinterpret_cast<const char*>(it.src.base) + boff;
-        int64_t done = 0;
-        while (done < n) {
-          if (cur.index >= 0 && (cur.device != it.device || cur.fill == cap)) {
-            if (!flush()) return;
-          }
-          if (cur.index < 0 && !open_slot(it.device)) return;
-          const int64_t take = std::min(n - done, cap - cur.fill);
-          cur.d2h.push_back({src + done, cur.fill, take});
-          cur.writes.push_back({it.file, cur.fill, it.file_off + done, take});
-          cur.fill += take;
-          done += take;
+      if (box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn)) {
+        const int64_t take = std::min(n - c.done, cap - cur.fill);
+        if (take <= 0) return true;
+        const char* src = reinterpret_cast<const char*>(it.src.base) + boff + c.done;
+        cur.device = it.device;
+        cur.d2h.push_back({src, cur.fill, take});
+        cur.writes.push_back({it.file, cur.fill, it.file_off + c.done, take});
+        cur.fill += take;
+        c.done += take;
+        if (c.done == n) {
+          ++c.pos;
+          c.done = 0;
         }
-      } else {
-        std::vector<SubBox> subs;
-        split_box(it.src.off, it.ext, it.rank, it.itemsize, cap, subs);
-        int64_t payload = 0;
-        for (auto& sb : subs) {
-          if (cur.index >= 0 && (cur.device != it.device || cur.fill + sb.nbytes > cap ||
-                                 cur.packs.size() >= max_packs)) {
-            if (!flush()) return;
-          }
-          if (cur.index < 0 && !open_slot(it.device)) return;
-          tv_copy c{};
-          c.src = it.src;
-          std::memcpy(c.src.off, sb.off, sizeof(int64_t) * it.rank);
-          std::memcpy(c.ext, sb.ext, sizeof(int64_t) * it.rank);
-          c.rank = it.rank;
-          c.itemsize = it.itemsize;
-          // dst filled in submit() once the staging address is known
-          for (int d = 0; d < it.rank; ++d) {
-            c.dst.shape[d] = sb.ext[d];
-            c.dst.off[d] = 0;
-          }
-          cur.packs.push_back(c);
-          cur.pack_offs.push_back(cur.fill);
-          cur.writes.push_back({it.file, cur.fill, it.file_off + payload, sb.nbytes});
-          cur.fill += sb.nbytes;
-          payload += sb.nbytes;
-        }
+        continue;
+      }
+      if (!c.split) {
+        c.subs.clear();
+        split_box(it.src.off, it.ext, it.rank, it.itemsize, cap, c.subs);
+        c.sub_pos = 0;
+        c.split = true;
+      }
+      const SubBox& sb = c.subs[c.sub_pos];
+      if (cur.fill + sb.nbytes > cap || cur.packs.size() >= max_packs) return true;
+      tv_copy cp{};
+      cp.src = it.src;
+      std::memcpy(cp.src.off, sb.off, sizeof(int64_t) * it.rank);
+      std::memcpy(cp.ext, sb.ext, sizeof(int64_t) * it.rank);
+      cp.rank = it.rank;
+      cp.itemsize = it.itemsize;
+      for (int d = 0; d < it.rank; ++d) {
+        cp.dst.shape[d] = sb.ext[d];  // dst base set in submit() (staging address)
+        cp.dst.off[d] = 0;
+      }
+      cur.device = it.device;
+      cur.packs.push_back(cp);
+      cur.pack_offs.push_back(cur.fill);
+      cur.writes.push_back({it.file, cur.fill, it.file_off + c.done, sb.nbytes});
+      cur.fill += sb.nbytes;
+      c.done += sb.nbytes;
+      if (++c.sub_pos == c.subs.size()) {
+        ++c.pos;
+        c.done = 0;
+        c.split = false;
       }
     }
-    flush();
+    return true;
+  }
+
+  void produce() {
+    std::vector<int> active;
+    for (size_t k = 0; k < cursors_.size(); ++k)
+      if (!cursors_[k].finished()) active.push_back((int)k);
+    while (!active.empty() && !err_.failed.load()) {
+      std::vector<int> still;
+      for (int k : active) {
+        if (err_.failed.load()) return;
+        int s;
+        if (!free_slots_.pop(s)) return;
+        SaveSlot cur;
+        cur.index = s;
+        cur.lane = k;
+        if (!fill_slot(cursors_[k], cur)) return;
+        if (cur.fill == 0 && cur.writes.empty()) {
+          free_slots_.push(s);
+        } else if (!submit(cur)) {
+          return;
+        }
+        if (!cursors_[k].finished()) still.push_back(k);
+      }
+      active.swap(still);
+    }
   }
 
   bool submit(SaveSlot& s) {
@@ -636,13 +689,13 @@ class SaveRun {
       events_.push_back(ev);
     }
     s.ev = ev;
-    ready_.push(std::move(s));
+    lanes_[s.lane]->push(std::move(s));
     return true;
   }
 
-  void writer_loop() {
+  void writer_loop(int lane) {
     SaveSlot s;
-    while (ready_.pop(s)) {
+    while (lanes_[lane]->pop(s)) {
       if (!err_.failed.load()) {
         cudaError_t ce = cudaEventSynchronize(s.ev);
         if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("D2H/pack: ") + cudaGetErrorString(ce));
@@ -753,7 +806,9 @@ class SaveRun {
   tv_stats* stats_;
   std::unique_ptr<OutputState[]> outs_;
   Queue<int> free_slots_;
-  Queue<SaveSlot> ready_;
+  std::vector<std::unique_ptr<Queue<SaveSlot>>> lanes_;
+  std::vector<LaneCursor> cursors_;
+  std::vector<int> lane_of_;
   ErrorSlot err_;
   DirMaker dirs_;
   std::mutex ev_m_;

@@ -1,0 +1,175 @@
+"""Host-side planning (no GPU): the integer rules every stored byte depends on.
+
+Known-answer values are the reference's own frozen vectors (test_chunkstore.py:56-121,
+test_sharding.py:143-178); property tests compare with brute-force restatements.
+"""
+
+from __future__ import annotations
+
+import itertools
+import math
+import random
+
+import numpy as np
+import pytest
+
+import paper_2605_23066_b200 as tv
+from paper_2605_23066_b200 import chunkstore, save_pipeline
+from paper_2605_23066_b200.errors import ChunkStoreError, ShardingError, DivisibilityError, TopologyError
+
+
+@pytest.mark.parametrize("shape,dtype,target,expect", [
+    ((64, 64), "f32", 4096, (16, 64)),
+    ((8, 8), "f32", 4096, (8, 8)),
+    ((16, 16), "f32", 32 << 20, (16, 16)),
+    ((15,), "f32", 16, (1,)),
+    ((15,), "f32", 32, (5,)),
+    ((49,), "f64", 60, (7,)),
+    ((1, 1), "f64", 8, (1, 1)),
+])
+def test_choose_chunk_shape_known_answers(shape, dtype, target, expect):
+    assert tv.choose_chunk_shape(shape, dtype, target) == expect
+
+
+def test_choose_chunk_shape_rejects_target_below_itemsize():
+    with pytest.raises(ChunkStoreError):
+        tv.choose_chunk_shape((4,), "f64", 4)
+
+
+def test_choose_chunk_shape_properties():
+    rng = random.Random(5)
+    for _ in range(200):
+        shape = tuple(rng.choice([1, 2, 3, 4, 6, 8, 12, 16, 60]) for _ in range(rng.randint(1, 3)))
+        dtype = rng.choice(["f32", "f64", "i32", "u8", "bool", "bf16"])
+        isz = tv.dtypes.itemsize(dtype) if hasattr(tv, "dtypes") else None
+        from paper_2605_23066_b200.dtypes import itemsize
+
+        isz = itemsize(dtype)
+        target = rng.choice([isz, 16, 64, 256, 4096])
+        got = tv.choose_chunk_shape(shape, dtype, target)
+        assert all(s % c == 0 for s, c in zip(shape, got))
+        grids = itertools.product(*[[d for d in range(1, s + 1) if s % d == 0] for s in shape])
+        if any(math.prod(g) * isz <= target for g in grids):
+            assert math.prod(got) * isz <= target
+        else:
+            assert got == (1,) * len(shape)
+
+
+@pytest.mark.parametrize("shard,n,expect", [
+    ((16, 16), 1, (16, 16)), ((1024,), 4, (256,)), ((10,), 4, (1,)), ((8, 4), 4, (2, 4)),
+    ((4, 16), 2, (4, 8)),
+])
+def test_derive_write_chunk_known_answers(shard, n, expect):
+    got = chunkstore.derive_write_chunk(shard, n)
+    assert got == expect
+    # every ceil-division segment boundary falls on a chunk boundary
+    ax = tv.sharding.segment_axis(shard) if hasattr(tv, "sharding") else None
+    from paper_2605_23066_b200.sharding import segment_axis
+
+    ax = segment_axis(shard)
+    step = -(-shard[ax] // n)
+    for o in range(n):
+        lo = min(o * step, shard[ax])
+        assert lo % got[ax] == 0
+
+
+def _shard(extent):
+    mesh = tv.Mesh.create([("data", 1)], 1)
+    return tv.shards_of(tv.Sharding(mesh, tv.PartitionSpec.of(None), (extent,)))[0]
+
+
+def test_replica_segments_known_answers():
+    assert tv.replica_segments(_shard(1024), 4, 1) == ((256, 256),)
+    assert tv.replica_segments(_shard(77), 1, 0) == ((0, 77),)
+    sizes = [0 if (s := tv.replica_segments(_shard(10), 4, o)) is None else s[0][1] for o in range(4)]
+    assert sizes == [3, 3, 3, 1]
+    mesh = tv.Mesh.create([("data", 1)], 1)
+    shard = tv.shards_of(tv.Sharding(mesh, tv.PartitionSpec.of(None, None), (4, 16)))[0]
+    assert tv.replica_segments(shard, 2, 0) == ((0, 4), (0, 8))
+    with pytest.raises(ShardingError):
+        tv.replica_segments(shard, 2, 2)
+
+
+def _random_sharding(rng):
+    shape, axes, entries, devices = [], [], [], 1
+    for dim in range(rng.randint(1, 3)):
+        s = rng.choice([1, 2, 4, 8, 12])
+        shape.append(s)
+        k = rng.choice([d for d in (1, 2, 4) if s % d == 0])
+        if k > 1:
+            axes.append((f"a{dim}", k))
+            entries.append(f"a{dim}")
+            devices *= k
+        else:
+            entries.append(None)
+    if rng.random() < 0.5:
+        axes.append(("rep", 2))
+        devices *= 2
+    if not axes:
+        axes = [("solo", 1)]
+    P = rng.choice([p for p in (1, 2, 4) if devices % p == 0])
+    mesh = tv.Mesh.create(axes, P, "rep" if any(a == "rep" for a, _ in axes) else None)
+    return tv.Sharding(mesh, tv.PartitionSpec(tuple(entries)), tuple(shape)), P
+
+
+@pytest.mark.parametrize("replica_parallel", [False, True])
+def test_write_pieces_tile_the_array_exactly_once(replica_parallel):
+    rng = random.Random(11)
+    for _ in range(150):
+        s, P = _random_sharding(rng)
+        boxes = []
+        for p in range(P):
+            for ranges, dev in save_pipeline.write_pieces_for_process(s, s.global_shape, p, replica_parallel):
+                boxes.append(ranges)
+                # the device that sources the piece holds it and lives on the process
+                assert s.mesh.process_of(dev) == p
+                holder = dict((sh.device, sh.ranges) for sh in tv.shards_of(s))[dev]
+                assert all(ho <= o and o + e <= ho + he for (o, e), (ho, he) in zip(ranges, holder))
+        counts = np.zeros(s.global_shape, np.int32)
+        for r in boxes:
+            counts[tuple(slice(o, o + e) for o, e in r)] += 1
+        assert (counts == 1).all()
+
+
+def test_storage_meta_replica_parallel_aligns_chunks():
+    mesh = tv.Mesh.create([("replica", 2), ("fsdp", 4)], 8, "replica")
+    s = tv.Sharding(mesh, tv.PartitionSpec.of("fsdp", None), (4096, 4096))
+    leaf = tv.treemodel.AbstractLeaf("array", (4096, 4096), "bf16")
+    meta = save_pipeline.storage_meta_for(leaf, s, tv.SaveOptions(replica_parallel=True))
+    # q (4096,4096) on 2x4, replica-parallel -> (1024, 2048) chunks
+    assert meta.shard_shape == (1024, 4096)
+    assert meta.write_chunk == (1024, 2048)
+
+
+def test_plan_fetches_whole_vs_subchunk():
+    meta = chunkstore.ArrayStorageMetadata((256, 64), "f32", (16, 16), (16, 16), (4, 16), "per_leaf")
+    entry = {"chunks": {f"{i}.{j}": {"p": 0} for i in range(16) for j in range(4)}}
+    # a (4, 64) row band needs one (4,16) subchunk from each of 4 chunks
+    f = chunkstore.plan_fetches("ck", "m/w", entry, meta, [((8, 4), (0, 64))])
+    assert [x.nbytes for x in f] == [4 * 16 * 4] * 4
+    assert all(x.op == "get_range" for x in f)
+    # the union of four bands covering a chunk fetches the whole chunk once
+    reqs = [((r, 4), (0, 64)) for r in (0, 4, 8, 12)]
+    f = chunkstore.plan_fetches("ck", "m/w", entry, meta, reqs)
+    assert [x.nbytes for x in f] == [16 * 16 * 4] * 4 and all(x.op == "get" for x in f)
+
+
+def test_mesh_and_topology_validation():
+    with pytest.raises(ShardingError):
+        tv.Mesh.create([("a", 3)], 2)
+    mesh = tv.Mesh.create([("a", 2)], 2)
+    with pytest.raises(DivisibilityError):
+        tv.Sharding(mesh, tv.PartitionSpec.of("a"), (3,)).check_divisible()
+    with pytest.raises(TopologyError):
+        tv.validate_topology(tv.sharding.describe_mesh(mesh) | {"devices": [1, 0]}, mesh)
+
+
+def test_fs_listing_matches_full_walk(tmp_path):
+    backend = tv.FilesystemBackend(tmp_path)
+    store = backend.store()
+    for key in ["a/ck/x", "a/ck/y/z", "a/ckx/w", "a/c", "b/ck/x", "a/ck.tmp.1/q"]:
+        store.put(key, b"1")
+    (tmp_path / "a" / "ck" / "p.partial").write_bytes(b"x")
+    everything = sorted(k for k in backend._list(""))
+    for prefix in ["", "a/", "a/ck/", "a/ck", "a/c", "b", "zz/", "a/ck/y/"]:
+        assert backend._list(prefix) == [k for k in everything if k.startswith(prefix)], prefix
