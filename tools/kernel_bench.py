@@ -1,0 +1,129 @@
+"""Box-copy kernel microbenchmark (the pack / unpack / snapshot kernel of the data path).
+
+    python tools/kernel_bench.py [--case snapshot|rp_pack|reshard_unpack|all] [--layers L] [--reps R]
+
+Cases (Llama-3-8B shapes, one GPU):
+  snapshot        every shard of an FSDP-8 rank's state (10 GB) -> one arena, contiguous boxes
+  rp_pack         C3 replica-parallel save: each (rows/4, cols) shard's column half
+                  (a strided 2-D box: run = cols/2 elements) packed chunk-major
+  reshard_unpack  C4 restore scatter: row-block chunks into (replica x fsdp) target shards
+Each case is ONE launch for the whole batch; time = CUDA events on the launching stream,
+median of R after 3 warm-ups.  Algorithmic bytes = 2 x bytes moved (read + write).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2605_23066_b200 import chunkstore, native  # noqa: E402
+
+D, FFN, V, KV = 4096, 14336, 128256, 1024
+
+
+def shapes(layers):
+    out = [(V, D), (V, D), (D,)]
+    for _ in range(layers):
+        out += [(D, D), (KV, D), (KV, D), (D, D), (FFN, D), (FFN, D), (D, FFN), (D,), (D,)]
+    return out
+
+
+def table(pairs):
+    """pairs: (src_tensor, src_off, dst_tensor, dst_off, ext)"""
+    copies = np.zeros(len(pairs), native.COPY)
+    moved = 0
+    for j, (s, so, t, to, ext) in enumerate(pairs):
+        rank = len(ext)
+        chunkstore._fill_box(copies[j]["src"], s.data_ptr(), tuple(s.shape), so)
+        chunkstore._fill_box(copies[j]["dst"], t.data_ptr(), tuple(t.shape), to)
+        copies[j]["ext"][:rank] = ext
+        copies[j]["rank"] = rank
+        copies[j]["itemsize"] = s.element_size()
+        moved += int(np.prod(ext)) * s.element_size()
+    return copies, moved
+
+
+def make_case(case, layers, fsdp=8):
+    dev = torch.device("cuda", 0)
+    pairs = []
+    keep = []
+    for tree, dt in (("params", torch.bfloat16), ("mu", torch.float32), ("nu", torch.float32)):
+        for shp in shapes(layers):
+            if case == "snapshot":
+                src = torch.randn((shp[0] // fsdp,) + shp[1:], device=dev).to(dt)
+                dst = torch.empty_like(src)
+                pairs.append((src, (0,) * src.dim(), dst, (0,) * src.dim(), tuple(src.shape)))
+                keep += [src, dst]
+            elif case == "rp_pack":
+                # 2x4 mesh, fsdp on dim 0: shard (rows/4, cols); replica r writes column half r
+                rows = shp[0] // 4
+                src = torch.randn((rows,) + shp[1:], device=dev).to(dt)
+                if len(shp) == 1:
+                    half = rows // 2
+                    dst = torch.empty((half,), device=dev, dtype=dt)
+                    pairs.append((src, (half,), dst, (0,), (half,)))
+                else:
+                    ext = (rows, shp[1] // 2) if shp[1] >= rows else (rows // 2, shp[1])
+                    off = (0, shp[1] // 2) if shp[1] >= rows else (rows // 2, 0)
+                    dst = torch.empty(ext, device=dev, dtype=dt)
+                    pairs.append((src, off, dst, (0, 0), ext))
+                keep += [src, dst]
+            elif case == "reshard_unpack":
+                # chunk = rows/8 block (from storage, contiguous) -> target shard rows/2 at an offset
+                crow = shp[0] // 8
+                chunk = torch.randn((crow,) + shp[1:], device=dev).to(dt)
+                target = torch.empty((shp[0] // 2,) + shp[1:], device=dev, dtype=dt)
+                for k in range(4):
+                    pairs.append((chunk, (0,) * chunk.dim(), target, (k * crow,) + (0,) * (chunk.dim() - 1),
+                                  tuple(chunk.shape)))
+                keep += [chunk, target]
+    copies, moved = table(pairs)
+    return copies, moved, keep
+
+
+def run(case, layers, reps, fsdp=8):
+    copies, moved, keep = make_case(case, layers, fsdp)
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        native.copy_boxes(0, copies, stream.cuda_stream)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        native.copy_boxes(0, copies, stream.cuda_stream)
+        b.record(stream)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = statistics.median(times)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    achieved = 2 * moved / (ms / 1e3) / 1e9
+    del keep
+    torch.cuda.empty_cache()
+    return {"case": case, "copies": len(copies), "bytes_moved": moved, "ms": round(ms, 3),
+            "achieved_GBps": round(achieved, 1), "peak_GBps": peak, "frac": round(achieved / peak, 4)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="all")
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--reps", type=int, default=10)
+    args = ap.parse_args()
+    cases = ["snapshot", "rp_pack", "reshard_unpack"] if args.case == "all" else [args.case]
+    for c in cases:
+        print(json.dumps(run(c, args.layers, args.reps)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
