@@ -402,15 +402,13 @@ def kernel_roofline(tv, native, state, rt, d) -> dict:
         offs.append(cur)
         cur += (t.numel() * t.element_size() + 255) & ~255
     arena = torch.empty(cur, dtype=torch.uint8, device=f"cuda:{gpu}")
-    copies = np.zeros(len(regions), native.COPY)
-    for j, (t, off) in enumerate(zip(regions, offs)):
-        shape = tuple(t.shape)
-        rank = len(shape)
-        chunkstore._fill_box(copies[j]["src"], t.data_ptr(), shape, (0,) * rank)
-        chunkstore._fill_box(copies[j]["dst"], arena.data_ptr() + off, shape, (0,) * rank)
-        copies[j]["ext"][:rank] = shape
-        copies[j]["rank"] = rank
-        copies[j]["itemsize"] = t.element_size()
+    base = arena.data_ptr()
+    copies = native.copy_table(
+        [t.data_ptr() for t in regions], [tuple(t.shape) for t in regions],
+        [(0,) * t.dim() for t in regions], [base + o for o in offs], [tuple(t.shape) for t in regions],
+        [(0,) * t.dim() for t in regions], [tuple(t.shape) for t in regions],
+        [t.element_size() for t in regions],
+    )
     stream = torch.cuda.current_stream(gpu)
     for _ in range(3):
         native.copy_boxes(gpu, copies, stream.cuda_stream)

@@ -522,17 +522,12 @@ def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, 
     root = backend.native_root()
     stats = None
     if pending:
-        items = np.zeros(len(pending), native.WRITE_ITEM)
-        for j, p in enumerate(pending):
-            rec = items[j]
-            _fill_box(rec["src"], p.region.address, p.region.shape, p.box_off)
-            rank = len(p.ext)
-            rec["ext"][:rank] = p.ext
-            rec["rank"] = rank
-            rec["itemsize"] = p.itemsize
-            rec["file"] = out_index[p.key]
-            rec["device"] = p.region.gpu
-            rec["file_off"] = p.file_off
+        items = native.write_table(
+            [p.region.address for p in pending], [p.region.shape for p in pending],
+            [p.box_off for p in pending], [p.ext for p in pending], [p.itemsize for p in pending],
+            [out_index[p.key] for p in pending], [p.region.gpu for p in pending],
+            [p.file_off for p in pending],
+        )
         outputs = np.zeros(len(out_keys), native.OUTPUT)
         outputs["size"] = sizes
         host_bufs: list[np.ndarray] = []
@@ -754,49 +749,50 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
                 f"chunk object {it.fetch.key!r} has {size} bytes, expected {it.fetch.nbytes}"
             )
     ritems = np.zeros(len(items), native.READ_ITEM)
-    copies_list = []
+    direct_dst = np.zeros(len(items), np.uint64)
+    first_copy = np.zeros(len(items), np.int32)
+    n_copies = np.zeros(len(items), np.int32)
+    cols: dict[str, list] = {k: [] for k in ("sb", "ss", "so", "db", "ds", "do", "ext", "isz")}
     for j, it in enumerate(items):
         f = it.fetch
-        rec = ritems[j]
-        rec["input"] = input_index[f.key]
-        rec["device"] = it.reader_gpu
-        rec["in_off"] = f.file_off
-        rec["nbytes"] = f.nbytes
         fetched = tuple(zip(f.origin, f.shape))
         direct = None
         for d in it.consumers:
             if d.gpu != it.reader_gpu:
                 continue
-            inside = all(
-                do <= fo and fo + fe <= do + de for (fo, fe), (do, de) in zip(fetched, d.ranges)
-            )
-            if not inside:
+            if not all(do <= fo and fo + fe <= do + de for (fo, fe), (do, de) in zip(fetched, d.ranges)):
                 continue
             dshape = tuple(e for _, e in d.ranges)
             doff = tuple(fo - do for (fo, _), (do, _) in zip(fetched, d.ranges))
             if box_is_contiguous(dshape, doff, f.shape):
                 direct = d
-                rec["direct_dst"] = d.address + box_flat_offset(dshape, doff) * d.itemsize
+                direct_dst[j] = d.address + box_flat_offset(dshape, doff) * d.itemsize
                 break
-        first = len(copies_list)
+        first_copy[j] = len(cols["ext"])
         for d in it.consumers:
             if d is direct:
                 continue
             hit = _intersect(fetched, d.ranges)
             if hit is None:
                 continue
-            c = np.zeros((), native.COPY)
-            rank = len(f.shape)
-            _fill_box(c["src"], 0, f.shape, tuple(h - o for (h, _), o in zip(hit, f.origin)))
-            _fill_box(c["dst"], d.address, tuple(e for _, e in d.ranges),
-                      tuple(h - o for (h, _), (o, _) in zip(hit, d.ranges)))
-            c["ext"][:rank] = [e for _, e in hit]
-            c["rank"] = rank
-            c["itemsize"] = d.itemsize
-            copies_list.append(c)
-        rec["first_copy"] = first
-        rec["n_copies"] = len(copies_list) - first
-    copies = np.array(copies_list, native.COPY) if copies_list else np.zeros(0, native.COPY)
+            cols["sb"].append(0)
+            cols["ss"].append(f.shape)
+            cols["so"].append(tuple(h - o for (h, _), o in zip(hit, f.origin)))
+            cols["db"].append(d.address)
+            cols["ds"].append(tuple(e for _, e in d.ranges))
+            cols["do"].append(tuple(h - o for (h, _), (o, _) in zip(hit, d.ranges)))
+            cols["ext"].append(tuple(e for _, e in hit))
+            cols["isz"].append(d.itemsize)
+        n_copies[j] = len(cols["ext"]) - first_copy[j]
+    ritems["input"] = [input_index[it.fetch.key] for it in items]
+    ritems["device"] = [it.reader_gpu for it in items]
+    ritems["in_off"] = [it.fetch.file_off for it in items]
+    ritems["nbytes"] = [it.fetch.nbytes for it in items]
+    ritems["direct_dst"] = direct_dst
+    ritems["first_copy"] = first_copy
+    ritems["n_copies"] = n_copies
+    copies = native.copy_table(cols["sb"], cols["ss"], cols["so"], cols["db"], cols["ds"], cols["do"],
+                               cols["ext"], cols["isz"])
     cfg = engine_cfg or native.EngineConfig()
     with native.engine_lease(cfg, concurrent) as eng:
         stats = eng.load(ritems, inputs, copies)

@@ -136,6 +136,53 @@ def _ptr(arr: np.ndarray) -> int:
     return arr.ctypes.data if arr.size else 0
 
 
+# ---- descriptor tables (vectorised column writes) --------------------------------------
+
+
+def pad_rows(rows: Sequence[Sequence[int]]) -> np.ndarray:
+    """(n, MAX_RANK) int64 array of per-dimension values, zero padded."""
+    out = np.zeros((len(rows), MAX_RANK), np.int64)
+    for i, r in enumerate(rows):
+        if r:
+            out[i, : len(r)] = r
+    return out
+
+
+def copy_table(src_base, src_shape, src_off, dst_base, dst_shape, dst_off, ext, itemsize) -> np.ndarray:
+    """COPY table from per-copy lists (bases ints, shapes/offsets/extents tuples)."""
+    n = len(ext)
+    t = np.zeros(n, COPY)
+    if n == 0:
+        return t
+    t["src"]["base"] = np.asarray(src_base, np.uint64)
+    t["src"]["shape"] = pad_rows(src_shape)
+    t["src"]["off"] = pad_rows(src_off)
+    t["dst"]["base"] = np.asarray(dst_base, np.uint64)
+    t["dst"]["shape"] = pad_rows(dst_shape)
+    t["dst"]["off"] = pad_rows(dst_off)
+    t["ext"] = pad_rows(ext)
+    t["rank"] = [len(e) for e in ext]
+    t["itemsize"] = itemsize
+    return t
+
+
+def write_table(src_base, src_shape, src_off, ext, itemsize, file, device, file_off) -> np.ndarray:
+    n = len(ext)
+    t = np.zeros(n, WRITE_ITEM)
+    if n == 0:
+        return t
+    t["src"]["base"] = np.asarray(src_base, np.uint64)
+    t["src"]["shape"] = pad_rows(src_shape)
+    t["src"]["off"] = pad_rows(src_off)
+    t["ext"] = pad_rows(ext)
+    t["rank"] = [len(e) for e in ext]
+    t["itemsize"] = itemsize
+    t["file"] = file
+    t["device"] = device
+    t["file_off"] = file_off
+    return t
+
+
 # ---- kernels ----------------------------------------------------------------------------
 
 

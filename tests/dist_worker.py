@@ -1,0 +1,132 @@
+"""torchrun worker for the one-process-per-GPU runtime (tests/test_distributed.py).
+
+    torchrun --nproc-per-node 2 tests/dist_worker.py <mode> <dir>
+
+mode "coord" (CPU, gloo): barriers, leader broadcast, step catalog, per-rank write plans.
+mode "datapath" (GPU): save the fsdp case from device shards on 2 ranks, compare every
+stored file with the oracle, then reshard-restore onto (replica 2 x fsdp 1) through the
+IPC-mapped read-once fan-out and compare every local shard with the oracle.
+Exit code 0 = pass.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+
+def coord(base: str) -> None:
+    import torch.distributed as dist
+
+    import paper_2605_23066_b200 as tv
+    from paper_2605_23066_b200 import save_pipeline
+
+    dist.init_process_group("gloo")
+    backend = tv.FilesystemBackend(base)
+    rt = tv.DistributedRuntime(backend)
+    rank, world = rt.rank, rt.process_count
+    ctx = rt.local
+    ctx.barrier("a")
+    got = ctx.leader_broadcast("nonce", b"abc" if rank == 0 else None)
+    assert got == b"abc", got
+    if rank == 0:
+        for step, final in ((1, True), (2, True), (3, False)):
+            store = backend.store()
+            store.put(f"run/step_{step:08d}/x", b"1")
+            if final:
+                store.put(f"run/step_{step:08d}/global_metadata.json", b"{}")
+    ctx.barrier("written")
+    ck = tv.Checkpointer(rt, "run")
+    assert ck.all_steps() == [1, 2], ck.all_steps()
+    assert tv.latest_step(rt, "run") == 2
+    # per-rank write plan: each rank persists exactly its own shards
+    mesh = tv.Mesh.create([("fsdp", world)], process_count=world)
+    s = tv.Sharding(mesh, tv.PartitionSpec.of("fsdp", None), (8 * world, 4))
+    pieces = save_pipeline.write_pieces_for_process(s, s.global_shape, rank, False)
+    assert pieces == [(((8 * rank, 8), (0, 4)), rank)], pieces
+    gathered = rt.all_gather_object(pieces)
+    assert len(gathered) == world
+    ctx.barrier("done")
+    dist.destroy_process_group()
+
+
+def datapath(base: str) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import cases
+    import paper_2605_23066_b200 as tv
+    import treevault_oracle as orc
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    gpu = local % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dist.init_process_group("gloo")
+    backend = tv.FilesystemBackend(base)
+    rt = tv.DistributedRuntime(backend, gpu=gpu)
+    world = rt.process_count
+    rng = np.random.default_rng(3)
+    tree = {"state": cases.llama_like(rng, layers=1, d=32, ffn=48, vocab=40, kv=8)}
+    specs = {"state": cases.fsdp_shardings(tree["state"], [("fsdp", world)], world)}
+    leaves = dict(cases.leaf_paths(tree["state"]))
+    shardings, state = {}, {}
+    for path, spec in specs["state"].items():
+        axes, P, ra, entries = spec
+        mesh = tv.Mesh.create(list(axes), process_count=P, replica_axis=ra)
+        leaf = leaves[path]
+        s = tv.Sharding(mesh, tv.PartitionSpec(tuple(entries)), leaf[2].shape)
+        shardings[path] = s
+        node = state
+        parts = path.split("/")
+        for p in parts[:-1]:
+            node = node.setdefault(p, {})
+        node[parts[-1]] = tv.device_put(tv.DenseArray(leaf[1], leaf[2]), s, rt)
+    for sync in (True, False):
+        path = f"ck/run_{int(sync)}"
+        tv.save_checkpoint(rt, path, {"state": state}, {"state": shardings},
+                           tv.SaveOptions(sync=sync)).wait()
+        rt.local.barrier(f"saved{sync}")
+        if rt.rank == 0:
+            expect = orc.expected_checkpoint(tree, specs, {}, world, "fs", path=path)
+            got = backend.dump()
+            got = {k: v for k, v in got.items() if k.startswith(path + "/")}
+            assert sorted(got) == sorted(expect), sorted(set(got) ^ set(expect))
+            for k, v in expect.items():
+                assert got[k] == v, k
+    # reshard restore onto (replica world x fsdp 1): every chunk needed by every rank
+    mesh2 = tv.Mesh.create([("replica", world), ("fsdp", 1)], process_count=world, replica_axis="replica")
+    abstract = {}
+    for path, leaf in leaves.items():
+        s2 = tv.Sharding(mesh2, tv.PartitionSpec(("fsdp",) + (None,) * (leaf[2].ndim - 1)), leaf[2].shape)
+        node = abstract
+        parts = path.split("/")
+        for p in parts[:-1]:
+            node = node.setdefault(p, {})
+        node[parts[-1]] = tv.AbstractLeaf("array", leaf[2].shape, leaf[1], s2)
+    before = backend.counters(f"process_{rt.rank}").payload_bytes_read
+    out = tv.load_checkpoint(rt, "ck/run_1", {"state": abstract})
+    read = backend.counters(f"process_{rt.rank}").payload_bytes_read - before
+    total_read = rt.all_gather_object(read)
+    stored = sum(leaf[2].nbytes for leaf in leaves.values())
+    assert sum(total_read) == stored, (total_read, stored)   # read once across ranks
+    for path, leaf in leaves.items():
+        node = out["state"]
+        for p in path.split("/"):
+            node = node[p]
+        assert sorted(node.shards) == [rt.rank], node.shards.keys()
+        got = tv.DenseArray(leaf[1], node.shards[rt.rank]).tobytes()
+        assert got == leaf[2].tobytes(), path
+    rt.local.barrier("done")
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    mode, base = sys.argv[1], sys.argv[2]
+    {"coord": coord, "datapath": datapath}[mode](base)
+    print(f"rank {os.environ.get('RANK')} ok")

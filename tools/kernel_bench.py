@@ -39,16 +39,13 @@ def shapes(layers):
 
 def table(pairs):
     """pairs: (src_tensor, src_off, dst_tensor, dst_off, ext)"""
-    copies = np.zeros(len(pairs), native.COPY)
-    moved = 0
-    for j, (s, so, t, to, ext) in enumerate(pairs):
-        rank = len(ext)
-        chunkstore._fill_box(copies[j]["src"], s.data_ptr(), tuple(s.shape), so)
-        chunkstore._fill_box(copies[j]["dst"], t.data_ptr(), tuple(t.shape), to)
-        copies[j]["ext"][:rank] = ext
-        copies[j]["rank"] = rank
-        copies[j]["itemsize"] = s.element_size()
-        moved += int(np.prod(ext)) * s.element_size()
+    copies = native.copy_table(
+        [s.data_ptr() for s, _, _, _, _ in pairs], [tuple(s.shape) for s, _, _, _, _ in pairs],
+        [so for _, so, _, _, _ in pairs], [t.data_ptr() for _, _, t, _, _ in pairs],
+        [tuple(t.shape) for _, _, t, _, _ in pairs], [to for _, _, _, to, _ in pairs],
+        [e for _, _, _, _, e in pairs], [s.element_size() for s, _, _, _, _ in pairs],
+    )
+    moved = sum(int(np.prod(e)) * s.element_size() for s, _, _, _, e in pairs)
     return copies, moved
 
 
