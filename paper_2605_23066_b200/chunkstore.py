@@ -286,21 +286,21 @@ class AggregatedManifest:
 
 @dataclass
 class DeviceRegion:
-    """Where the values of one box live on a GPU: ``tensor`` (contiguous, row-major)
-    holds the box at offset ``origin`` (per-dimension).  A shard, a global array and a
-    packed snapshot buffer are all DeviceRegions — no copy is made to describe a box."""
+    """Where the values of one box live on a GPU: the contiguous row-major array at
+    ``address`` of extents ``shape`` holds the box at offset ``origin``.  A shard, a
+    global array and a slice of a packed snapshot arena are all DeviceRegions — no copy
+    (and no tensor view) is made to describe a box.  ``owner`` keeps the memory alive."""
 
-    tensor: Any
+    address: int
+    shape: tuple[int, ...]
     origin: tuple[int, ...]
     gpu: int
+    owner: Any = None
 
-    @property
-    def shape(self) -> tuple[int, ...]:
-        return tuple(int(s) for s in self.tensor.shape)
-
-    @property
-    def address(self) -> int:
-        return int(self.tensor.data_ptr())
+    @classmethod
+    def of(cls, tensor, origin: tuple[int, ...]) -> "DeviceRegion":
+        return cls(int(tensor.data_ptr()), tuple(int(s) for s in tensor.shape), tuple(origin),
+                   tensor.device.index, tensor)
 
 
 def as_device_region(values: Any, extents: tuple[int, ...], dtype: str, gpu: int | None = None) -> DeviceRegion:
@@ -329,7 +329,7 @@ def as_device_region(values: Any, extents: tuple[int, ...], dtype: str, gpu: int
     if tuple(t.shape) != tuple(extents):
         raise AlignmentError(f"shard buffer shape {tuple(t.shape)} does not match extents {extents}")
     t = t.contiguous()
-    return DeviceRegion(t, (0,) * len(extents), t.device.index)
+    return DeviceRegion.of(t, (0,) * len(extents))
 
 
 def _fill_box(rec: np.ndarray, base: int, shape: Sequence[int], off: Sequence[int]) -> None:

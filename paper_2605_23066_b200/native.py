@@ -308,6 +308,8 @@ class EngineConfig:
     def threads_for(self, concurrent: int) -> int:
         if self.threads:
             return self.threads
+        # engines of other ranks on this box (torchrun) share the host cores too
+        concurrent = max(concurrent, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
         cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
         return max(2, (cores or 8) // max(1, concurrent))
 
