@@ -174,7 +174,7 @@ class Dist:
 # -- workload ------------------------------------------------------------------------------------
 
 
-def build_state(tv, rt, mesh, leaves, seed=0):
+def build_state(tv, rt, mesh, leaves, seed=0, spec_fn=None):
     """Device shards of every leaf for the devices this process owns (synthetic values
     generated on the GPU: N(0, 0.02) params, N(0, 1e-3) mu, N(0,1e-3)^2 nu)."""
     import torch
@@ -183,14 +183,26 @@ def build_state(tv, rt, mesh, leaves, seed=0):
     trees, shardings = {}, {}
     owned = set(rt.addressable_processes)
     for i, (tree, path, shape, dtype) in enumerate(leaves):
-        spec = ("fsdp",) + (None,) * (len(shape) - 1)
+        spec = (spec_fn or (lambda s: ("fsdp",) + (None,) * (len(s) - 1)))(shape)
+        if spec is None:  # unsharded leaf: one global array on process 0's GPU
+            gpu = rt.gpu_of_process(0)
+            gen.manual_seed(1000 * (i + 1) + seed)
+            t = torch.empty(shape, dtype=torch.float32 if dtype == "f32" else torch.bfloat16, device=f"cuda:{gpu}")
+            t.normal_(0.0, 1.0, generator=gen)
+            node = trees.setdefault(tree, {})
+            parts = path.split("/")
+            for p in parts[:-1]:
+                node = node.setdefault(p, {})
+            node[parts[-1]] = tv.DenseArray(dtype, t)
+            continue
         s = tv.Sharding(mesh, tv.PartitionSpec(spec), shape)
         shards = {}
         for sh in tv.shards_of(s):
             if mesh.process_of(sh.device) not in owned:
                 continue
             gpu = rt.gpu_of_device(sh.device)
-            gen.manual_seed(1000 * (i + 1) + sh.device + seed)
+            # replicas of a range hold identical values (seeded by the range, not the device)
+            gen.manual_seed(1000 * (i + 1) + sh.ranges[0][0] + seed)
             ext = tuple(e for _, e in sh.ranges)
             with torch.cuda.device(gpu):
                 t = torch.empty(ext, dtype=torch.float32 if dtype == "f32" else torch.bfloat16,
@@ -217,6 +229,88 @@ def _flatten_shardings(per_tree):
     return out
 
 
+class Workload:
+    """One benchmark configuration (BASELINE.json configs)."""
+
+    def __init__(self, tv, name, leaves, save_mesh, spec_fn, save_options, restore_mesh=None,
+                 restore_P=None, describe=""):
+        self.tv, self.name, self.leaves = tv, name, leaves
+        self.save_mesh, self.spec_fn, self.save_options = save_mesh, spec_fn, save_options
+        self.restore_mesh = restore_mesh          # None: restore onto the saved topology
+        self.restore_P = restore_P
+        self.describe = describe
+        self.tree_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
+
+    def shardings(self, mesh):
+        tv = self.tv
+        out = {}
+        for tree, path, shape, dtype in self.leaves:
+            spec = self.spec_fn(shape)
+            out[f"{tree}/{path}"] = None if spec is None else tv.Sharding(mesh, tv.PartitionSpec(spec), shape)
+        return out
+
+    def abstract(self):
+        tv = self.tv
+        sh = self.shardings(self.restore_mesh)
+        tree: dict = {}
+        for t, path, shape, dtype in self.leaves:
+            node = tree.setdefault(t, {})
+            parts = path.split("/")
+            for p in parts[:-1]:
+                node = node.setdefault(p, {})
+            node[parts[-1]] = tv.AbstractLeaf("array", shape, dtype, sh[f"{t}/{path}"])
+        return {"state": tree}
+
+
+def fsdp_spec(shape):
+    return ("fsdp",) + (None,) * (len(shape) - 1)
+
+
+def make_workload(tv, args, N) -> Workload:
+    dims = dict(LLAMA3_8B, layers=args.layers)
+    llama = llama_leaves(**dims)
+    cfg = args.config
+    if cfg == "c1":
+        leaves = [("model", f"a{i}", (4096, 4096), "f32") for i in range(4)]
+        mesh = tv.Mesh.create([("solo", 1)], process_count=1)
+        return Workload(tv, "c1", leaves, mesh, lambda s: None, tv.SaveOptions(sync=True),
+                        describe="C1 4 x (4096,4096) f32 unsharded, process 0 writes, sync save -> restore")
+    if cfg == "c2":
+        mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
+        return Workload(tv, "c2", llama, mesh, fsdp_spec, tv.SaveOptions(sync=True),
+                        describe=f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu, FSDP-{N} on dim 0, "
+                                 "sync save -> restore, per_leaf layout")
+    if cfg in ("c3", "c3ss"):
+        if N % 2:
+            raise SystemExit("c3 needs an even number of GPUs (replica 2 x fsdp N/2)")
+        mesh = tv.Mesh.create([("replica", 2), ("fsdp", N // 2)], process_count=N, replica_axis="replica")
+        rp = cfg == "c3"
+        return Workload(tv, cfg, llama, mesh, fsdp_spec, tv.SaveOptions(sync=True, replica_parallel=rp),
+                        describe=f"C3 Llama-3-8B on a 2x{N // 2} (replica x fsdp) mesh, "
+                                 f"{'replica-parallel' if rp else 'single-slice'} sync save -> restore")
+    if cfg == "c4":
+        if N % 2:
+            raise SystemExit("c4 needs an even number of GPUs")
+        Pr = args.restore_gpus or N
+        save_mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
+        rmesh = tv.Mesh.create([("replica", 2), ("fsdp", Pr // 2)], process_count=Pr, replica_axis="replica")
+        return Workload(tv, "c4", llama, save_mesh, fsdp_spec, tv.SaveOptions(sync=True), restore_mesh=rmesh,
+                        restore_P=Pr,
+                        describe=f"C4 Llama-3-8B saved 1x{N} (FSDP-{N}) -> restored onto 2x{Pr // 2} "
+                                 f"(replica x fsdp, {Pr} GPUs), read-once + NVLink fan-out")
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def open_runtime(tv, d, N, backend, gpus=None):
+    import torch
+
+    if d.on:
+        return tv.DistributedRuntime(backend)
+    visible = torch.cuda.device_count()
+    gpus = [g for g in (gpus if gpus is not None else range(N)) if g < visible] or [0]
+    return tv.SimulatedRuntime(N, backend, gpus=gpus)
+
+
 def run_ours(args) -> dict:
     import torch
 
@@ -233,19 +327,20 @@ def run_ours(args) -> dict:
         os.makedirs(base, exist_ok=True)
     d.barrier()
     backend = tv.FilesystemBackend(base)
-    if d.on:
-        rt = tv.DistributedRuntime(backend)
-    else:
-        rt = tv.SimulatedRuntime(N, backend, gpus=list(range(N)))
-    dims = dict(LLAMA3_8B)
-    dims["layers"] = args.layers
-    leaves = llama_leaves(**dims)
-    tree_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
-    mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
-    state, shardings = build_state(tv, rt, mesh, leaves)
+    wl = make_workload(tv, args, N)
+    P = wl.save_mesh.process_count
+    rt = open_runtime(tv, d, P, backend, gpus=list(range(N)))
+    rrt = rt
+    if wl.restore_P is not None and wl.restore_P != P:
+        if d.on:
+            raise SystemExit("a restore onto a different process count needs the threads runtime (no torchrun)")
+        rrt = tv.SimulatedRuntime(wl.restore_P, backend, gpus=list(range(min(N, wl.restore_P))))
+    state, shardings = build_state(tv, rt, wl.save_mesh, wl.leaves, spec_fn=wl.spec_fn)
+    abstract = wl.abstract() if wl.restore_mesh is not None else None
     torch.cuda.synchronize()
+    tree_bytes = wl.tree_bytes
 
-    def step(i: int, timed: bool):
+    def step(i: int):
         path = f"bench/step_{i:04d}"
         d.barrier()
         torch.cuda.synchronize()
@@ -254,27 +349,28 @@ def run_ours(args) -> dict:
         ev2 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         ev0.record()
-        tv.save_checkpoint(rt, path, state, shardings, tv.SaveOptions(sync=True)).wait()
+        tv.save_checkpoint(rt, path, state, shardings, wl.save_options).wait()
         ev1.record()
         t1 = time.perf_counter()
-        out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=mesh)
+        if abstract is None:
+            out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=wl.save_mesh)
+        else:
+            out = tv.load_checkpoint(rrt, path, abstract, tv.LoadOptions())
         ev2.record()
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         d.barrier()
         del out
-        save_ms = ev0.elapsed_time(ev1)
-        restore_ms = ev1.elapsed_time(ev2)
         if d.rank == 0:
             shutil.rmtree(os.path.join(base, path), ignore_errors=True)
         d.barrier()
-        return save_ms, restore_ms, (t1 - t0) * 1e3, (t2 - t1) * 1e3
+        return ev0.elapsed_time(ev1), ev1.elapsed_time(ev2), (t1 - t0) * 1e3, (t2 - t1) * 1e3
 
     for i in range(args.warmup):
-        step(i, False)
+        step(i)
 
-    # --- roofline probes (same run, same directory, after warm-up: the VM's first touch
-    # of fresh memory is slower than steady state) ----------------------------------------------
+    # roofline probes in the same run and directory, after warm-up (a VM's first touch of
+    # fresh memory is slower than steady state)
     probe = {}
     if d.rank == 0:
         nthreads = len(os.sched_getaffinity(0))
@@ -289,16 +385,21 @@ def run_ours(args) -> dict:
     probe["pcie_d2h_GBps_per_gpu"] = round(d2h, 2)
     probe["pcie_h2d_GBps_per_gpu"] = round(h2d, 2)
     d.barrier()
+
     clocks = ClockSampler()
     if d.rank == 0:
         clocks.start()
+    before = native.totals()
     saves, restores, walls = [], [], []
     for i in range(args.steps):
-        s_ms, r_ms, ws, wr = step(args.warmup + i, True)
+        s_ms, r_ms, ws, wr = step(args.warmup + i)
         saves.append(d.max(s_ms))
         restores.append(d.max(r_ms))
         walls.append(d.max(ws + wr))
+    after = native.totals()
     clock_info = clocks.stop() if d.rank == 0 else {}
+    kernels = d.sum(after["kernel_launches"] - before["kernel_launches"])
+    dmas = d.sum(after["dma_copies"] - before["dma_copies"])
     save_ms = statistics.mean(saves)
     restore_ms = statistics.mean(restores)
     step_ms = save_ms + restore_ms
@@ -306,11 +407,12 @@ def run_ours(args) -> dict:
     save_gbs = tree_bytes / (save_ms / 1e3) / 1e9
     restore_gbs = tree_bytes / (restore_ms / 1e3) / 1e9
 
-    # --- async-save blocking vs sync save ---------------------------------------------------------
+    # async-save blocking vs the sync save it replaces
     d.barrier()
     torch.cuda.synchronize()
+    async_opts = tv.SaveOptions(sync=False, replica_parallel=wl.save_options.replica_parallel)
     t0 = time.perf_counter()
-    handle = tv.save_checkpoint(rt, "bench/async", state, shardings, tv.SaveOptions(sync=False))
+    handle = tv.save_checkpoint(rt, "bench/async", state, shardings, async_opts)
     blocking_ms = d.max((time.perf_counter() - t0) * 1e3)
     handle.wait()
     async_total_ms = d.max((time.perf_counter() - t0) * 1e3)
@@ -318,17 +420,10 @@ def run_ours(args) -> dict:
     if d.rank == 0:
         shutil.rmtree(os.path.join(base, "bench"), ignore_errors=True)
 
-    # --- box-copy kernel roofline: device snapshot of the whole local state ---------------------
     kern = kernel_roofline(tv, native, state, rt, d)
-
-    # --- end to end through the host-array API ----------------------------------------------------
-    e2e = end_to_end(tv, rt, mesh, leaves, args, d, base)
+    e2e = end_to_end(tv, rt, wl, args, d, base) if not args.no_e2e else None
 
     peaks = measured_peaks()
-    binding = None
-    if d.rank == 0:
-        pcie_total = min(probe["pcie_d2h_GBps_per_gpu"], probe["pcie_h2d_GBps_per_gpu"]) * N
-        binding = min(probe["storage_write_GBps"], probe["storage_read_GBps"], pcie_total)
     result = {
         "metric": "checkpoint save+restore throughput (GB/s of tree bytes, save and restore each count once)",
         "value": round(value, 3),
@@ -343,14 +438,14 @@ def run_ours(args) -> dict:
         "dtype": "bf16+f32 bytes (pure data movement)",
         "data": "synthetic (random values generated on device, Llama-3-8B shapes)",
         "config": {
-            "workload": f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu, {len(leaves)} leaves, "
-                        f"{tree_bytes} bytes, FSDP-{N} on dim 0, sync save -> restore, per_leaf layout",
+            "workload": wl.describe + f", {len(wl.leaves)} leaves, {tree_bytes} bytes",
+            "config": wl.name,
             "layers": args.layers,
             "tree_bytes": tree_bytes,
             "storage": f"FilesystemBackend on {base} (tmpfs)",
-            "parallelism": f"fsdp{N}, one logical process per GPU",
+            "parallelism": f"{N} GPUs, one logical process per GPU" + (" (torchrun)" if d.on else " (threads runtime)"),
             "l2": "inputs (tree bytes) far larger than the 126 MB L2; no flush needed",
-            "timing": "CUDA events on the current stream around save and restore, max over ranks",
+            "timing": "CUDA events on the current stream around save and restore, barrier+sync both sides, max over ranks",
         },
         "save_GBps": round(save_gbs, 3),
         "restore_GBps": round(restore_gbs, 3),
@@ -363,21 +458,128 @@ def run_ours(args) -> dict:
         "io_roofline": None,
         "roofline": kern,
         "e2e": e2e,
-        "gpu_launches": None,
+        "gpu_launches": int(kernels + dmas),
+        "gpu_launches_breakdown": {
+            "box_copy_kernel": int(kernels),
+            "copy_engine_dma_by_libtvgpu": int(dmas),
+            "note": "contiguous chunk payloads move by copy-engine DMA issued by libtvgpu's engine "
+                    "(measured faster than SM-driven PCIe: profiles/r01_pcie_kernel_vs_ce.jsonl); "
+                    "strided boxes, snapshots and reshard scatters run box_copy_kernel",
+        },
         "clocks": clock_info,
     }
     if d.rank == 0:
+        pcie_d2h = probe["pcie_d2h_GBps_per_gpu"] * N
+        pcie_h2d = probe["pcie_h2d_GBps_per_gpu"] * N
+        save_peak = min(probe["storage_write_GBps"], pcie_d2h)
+        restore_peak = min(probe["storage_read_GBps"], pcie_h2d)
         result["io_roofline"] = {
-            "bound": "storage" if binding < min(probe["pcie_d2h_GBps_per_gpu"], probe["pcie_h2d_GBps_per_gpu"]) * N else "pcie",
-            "peak_GBps": round(binding, 2),
-            "save_frac": round(save_gbs / min(probe["storage_write_GBps"], probe["pcie_d2h_GBps_per_gpu"] * N), 4),
-            "restore_frac": round(restore_gbs / min(probe["storage_read_GBps"], probe["pcie_h2d_GBps_per_gpu"] * N), 4),
+            "bound": "storage" if probe["storage_write_GBps"] < pcie_d2h else "pcie",
+            "save_peak_GBps": round(save_peak, 2),
+            "restore_peak_GBps": round(restore_peak, 2),
+            "save_frac": round(save_gbs / save_peak, 4),
+            "restore_frac": round(restore_gbs / restore_peak, 4),
+            "step_frac": round(value / (2 / (1 / save_peak + 1 / restore_peak)), 4),
             **probe,
         }
         result["roofline"]["peak_source"] = peaks["source"]
-        result["gpu_launches"] = kern.get("launches_in_timed_region")
         if not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(args, sample_layers=args.cpu_layers)
+    return result
+
+
+def run_c5(args) -> dict:
+    """C5: Checkpointer async save every step (keep_last=3) inside a synthetic training
+    loop; reports the time the training loop is blocked in save_step."""
+    import torch
+
+    import paper_2605_23066_b200 as tv
+
+    d = Dist()
+    d.init()
+    N = d.world if d.on else args.gpus
+    torch.cuda.set_device(d.local)
+    base = args.dir
+    if d.rank == 0:
+        shutil.rmtree(base, ignore_errors=True)
+        os.makedirs(base, exist_ok=True)
+    d.barrier()
+    backend = tv.FilesystemBackend(base)
+    mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
+    rt = open_runtime(tv, d, N, backend, gpus=list(range(N)))
+    leaves = llama_leaves(**dict(LLAMA3_8B, layers=args.layers))
+    tree_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
+    state, shardings = build_state(tv, rt, mesh, leaves)
+    params = [t for p, leaf in tv.flatten(state["state"]["params"]) for t in leaf.shards.values()]
+    torch.cuda.synchronize()
+    # the synchronous save this replaces
+    sync_ms = []
+    for i in range(2):
+        d.barrier()
+        t0 = time.perf_counter()
+        tv.save_checkpoint(rt, f"sync/{i}", state, shardings, tv.SaveOptions(sync=True)).wait()
+        sync_ms.append(d.max((time.perf_counter() - t0) * 1e3))
+        d.barrier()
+        if d.rank == 0:
+            shutil.rmtree(os.path.join(base, "sync"), ignore_errors=True)
+    sync_save_ms = sync_ms[-1]
+    cycles = int(args.train_ms * 1.965e6)
+    ck = tv.Checkpointer(rt, "run", tv.RetentionPolicy(keep_last=3), tv.SaveOptions(sync=False))
+    blocking, waits, joins, gcs, bg = [], [], [], [], []
+    t_start = time.perf_counter()
+    for step in range(args.steps):
+        # synthetic training step: fixed GPU time + an in-place update of every param shard
+        torch.cuda._sleep(cycles)
+        for t in params:
+            t.mul_(0.999)
+        torch.cuda.synchronize()
+        d.barrier()
+        t0 = time.perf_counter()
+        handle = ck.save_step(step, state, shardings)
+        blocking.append(d.max((time.perf_counter() - t0) * 1e3))
+        waits.append(d.max(ck.last_wait_seconds * 1e3))
+        joins.append(d.max(ck.last_join_seconds * 1e3))
+        gcs.append(d.max(ck.last_gc_seconds * 1e3))
+        if step > 0:
+            tl = prev.handles[0].session.timeline
+            if "finalized" in tl and "snapshotted" in tl:
+                bg.append((tl["finalized"] - tl["snapshotted"]) * 1e3)
+        prev = handle
+    ck.wait()
+    loop_s = time.perf_counter() - t_start
+    kept = ck.all_steps()
+    assert kept == list(range(args.steps - 3, args.steps)), kept
+    snap = [b - w for b, w in zip(blocking, waits)]
+    steady = blocking[1:] or blocking
+    result = {
+        "metric": "async-save blocking time per training step (Checkpointer.save_step every step)",
+        "value": round(statistics.mean(steady), 2),
+        "unit": "ms",
+        "higher_is_better": False,
+        "n_gpus": N,
+        "steps": args.steps,
+        "config": {
+            "workload": f"C5 Checkpointer(keep_last=3, async) every step over {args.steps} steps, "
+                        f"Llama-3-8B {args.layers} layers ({tree_bytes} bytes) FSDP-{N}, synthetic "
+                        f"training step = {args.train_ms} ms GPU time + in-place param update",
+            "config": "c5",
+        },
+        "blocking_ms_mean": round(statistics.mean(steady), 2),
+        "blocking_ms_p50": round(statistics.median(steady), 2),
+        "blocking_ms_max": round(max(steady), 2),
+        "wait_on_previous_ms_mean": round(statistics.mean(waits[1:] or waits), 2),
+        "own_sync_phase_ms_mean": round(statistics.mean(snap[1:] or snap), 2),
+        "join_previous_ms_mean": round(statistics.mean(joins[1:] or joins), 2),
+        "retention_gc_ms_mean": round(statistics.mean(gcs[1:] or gcs), 2),
+        "background_save_ms_mean": round(statistics.mean(bg), 2) if bg else None,
+        "sync_save_ms": round(sync_save_ms, 2),
+        "blocking_frac_of_sync_save": round(statistics.mean(steady) / sync_save_ms, 4),
+        "loop_seconds": round(loop_s, 2),
+        "retained_steps": kept,
+    }
+    d.barrier()
+    if d.rank == 0:
+        shutil.rmtree(base, ignore_errors=True)
     return result
 
 
@@ -392,7 +594,7 @@ def kernel_roofline(tv, native, state, rt, d) -> dict:
     regions = []
     for tree in state.values():
         for path, leaf in tv.flatten(tree):
-            for dev, t in leaf.shards.items():
+            for dev, t in _device_tensors(leaf):
                 regions.append(t)
     gpu = regions[0].device.index
     regions = [t for t in regions if t.device.index == gpu]
@@ -439,23 +641,29 @@ def kernel_roofline(tv, native, state, rt, d) -> dict:
     }
 
 
-def end_to_end(tv, rt, mesh, leaves, args, d, base) -> dict:
+def _device_tensors(leaf):
+    return leaf.shards.items() if hasattr(leaf, "shards") else [(-1, leaf.data)]
+
+
+def end_to_end(tv, rt, wl, args, d, base) -> dict:
     """Same metric through the host-array API: inputs H2D from pinned host memory and the
     restored shards D2H into pinned host memory, inside the timed region.  Runs on a
     reduced-depth tree when host RAM cannot hold inputs + outputs + the checkpoint."""
     import torch
 
-    layers = args.e2e_layers
-    dims = dict(LLAMA3_8B)
-    dims["layers"] = layers
-    e_leaves = llama_leaves(**dims)
+    mesh = wl.save_mesh
+    if wl.name == "c1":
+        layers, e_leaves = 0, wl.leaves
+    else:
+        layers = args.e2e_layers
+        e_leaves = llama_leaves(**dict(LLAMA3_8B, layers=layers))
     # host copies of this process's shards (pinned), generated from the device state
-    state, shardings = build_state(tv, rt, mesh, e_leaves, seed=7)
+    state, shardings = build_state(tv, rt, mesh, e_leaves, seed=7, spec_fn=wl.spec_fn)
     host = {}
     local_bytes = 0
     for tree in state.values():
         for path, leaf in tv.flatten(tree):
-            for dev, t in leaf.shards.items():
+            for dev, t in _device_tensors(leaf):
                 h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
                 h.copy_(t)
                 host[(path, dev)] = h
@@ -469,15 +677,15 @@ def end_to_end(tv, rt, mesh, leaves, args, d, base) -> dict:
         t0 = time.perf_counter()
         for tree in state.values():  # H2D: inputs from pinned host memory
             for path, leaf in tv.flatten(tree):
-                for dev, t in leaf.shards.items():
+                for dev, t in _device_tensors(leaf):
                     t.copy_(host[(path, dev)], non_blocking=True)
         torch.cuda.synchronize()
         path = f"e2e/step_{i}"
-        tv.save_checkpoint(rt, path, state, shardings, tv.SaveOptions(sync=True)).wait()
+        tv.save_checkpoint(rt, path, state, shardings, wl.save_options).wait()
         out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=mesh)
         for tree in out.values():  # D2H: restored shards to pinned host memory
             for p, leaf in tv.flatten(tree):
-                for dev, t in leaf.shards.items():
+                for dev, t in _device_tensors(leaf):
                     host[(p, dev)].copy_(t, non_blocking=True)
         torch.cuda.synchronize()
         dt = d.max(time.perf_counter() - t0)
@@ -498,6 +706,7 @@ def end_to_end(tv, rt, mesh, leaves, args, d, base) -> dict:
         "d2h_bytes_per_step": int(total_local),
         "tree_bytes": tree_bytes,
         "layers": layers,
+        "config": wl.name,
         "api": "save_checkpoint(sync) + load_checkpoint with H2D of inputs / D2H of results (pinned)",
         "steps": args.e2e_steps,
     }
@@ -597,6 +806,10 @@ def main() -> None:
     ap.add_argument("--cpu-layers", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dir", default="/dev/shm/tvbench")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c3ss", "c4", "c5"])
+    ap.add_argument("--restore-gpus", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--train-ms", type=float, default=1000.0)
     args = ap.parse_args()
     if args.impl == "reference":
         d = Dist()
@@ -604,9 +817,17 @@ def main() -> None:
             return
         print(json.dumps(run_reference(args)))
         return
-    result = run_ours(args)
+    result = run_c5(args) if args.config == "c5" else run_ours(args)
     if Dist().rank == 0:
-        print(json.dumps(result))
+        print(json.dumps(result), flush=True)
+    try:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.barrier()
+            dist.destroy_process_group()
+    except Exception:  # noqa: BLE001 - teardown only
+        pass
 
 
 if __name__ == "__main__":

@@ -186,12 +186,32 @@ def write_table(src_base, src_shape, src_off, ext, itemsize, file, device, file_
 # ---- kernels ----------------------------------------------------------------------------
 
 
+# Process-wide counters of native work (bench.py reports the kernel launches and DMA
+# transfers its timed region issued).
+TOTALS = {"kernel_launches": 0, "dma_copies": 0, "bytes_device": 0, "bytes_storage": 0,
+          "bytes_packed": 0, "files": 0}
+_totals_lock = threading.Lock()
+
+
+def _account(stats) -> None:
+    with _totals_lock:
+        for k in TOTALS:
+            TOTALS[k] += int(stats[k])
+
+
+def totals() -> dict:
+    with _totals_lock:
+        return dict(TOTALS)
+
+
 def copy_boxes(device: int, copies: np.ndarray, stream: int = 0) -> None:
     """One batched box-copy launch on ``device``/``stream`` (COPY-dtype table)."""
     copies = np.ascontiguousarray(copies, dtype=COPY)
     if copies.size == 0:
         return
     check(lib().tv_copy_boxes(device, _ptr(copies), len(copies), stream), "tv_copy_boxes")
+    with _totals_lock:
+        TOTALS["kernel_launches"] += 1
 
 
 def enable_peer_access(gpus: Sequence[int]) -> None:
@@ -276,6 +296,7 @@ class Engine:
         outputs = np.ascontiguousarray(outputs, OUTPUT)
         rc = lib().tv_engine_save(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
                                   stats.ctypes.data)
+        _account(stats[0])
         check(rc, "tv_engine_save")
         return stats[0]
 
@@ -286,6 +307,7 @@ class Engine:
         copies = np.ascontiguousarray(copies, COPY)
         rc = lib().tv_engine_load(self._h, _ptr(items), len(items), _ptr(inputs), len(inputs),
                                   _ptr(copies), len(copies), stats.ctypes.data)
+        _account(stats[0])
         check(rc, "tv_engine_load")
         return stats[0]
 

@@ -1,0 +1,67 @@
+"""Engine pipeline sizing sweep: save + restore of a Llama-3-8B slice on one GPU for
+several (slot bytes, slot count, threads) settings.  Prints one JSON line per setting.
+
+    python tools/engine_sweep.py [--layers 8]
+"""
+
+import argparse
+import json
+import os
+import shutil
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2605_23066_b200 as tv  # noqa: E402
+from paper_2605_23066_b200 import native  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--reps", type=int, default=2)
+    args = ap.parse_args()
+    base = "/dev/shm/tvsweep"
+    shutil.rmtree(base, ignore_errors=True)
+    backend = tv.FilesystemBackend(base)
+    rt = tv.SimulatedRuntime(1, backend, gpus=[0])
+    leaves = bench.llama_leaves(**dict(bench.LLAMA3_8B, layers=args.layers))
+    mesh = tv.Mesh.create([("fsdp", 1)], process_count=1)
+    state, shardings = bench.build_state(tv, rt, mesh, leaves)
+    nbytes = sum(bench.nbytes(s, dt) for _, _, s, dt in leaves)
+    cores = len(os.sched_getaffinity(0))
+    settings = [
+        (8 << 20, 32, cores), (2 << 20, 32, cores), (4 << 20, 16, cores), (16 << 20, 16, cores),
+        (32 << 20, 8, cores), (8 << 20, 64, cores), (8 << 20, 32, cores // 2), (8 << 20, 32, cores + 8),
+    ]
+    i = 0
+    for slot, nslots, threads in settings:
+        rt.engine_config = native.EngineConfig(slot_bytes=slot, n_slots=nslots, threads=threads)
+        best_s = best_r = 0.0
+        for _ in range(args.reps + 1):
+            path = f"s/{i}"
+            i += 1
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tv.save_checkpoint(rt, path, state, shardings, tv.SaveOptions(sync=True)).wait()
+            t1 = time.perf_counter()
+            out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=mesh)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            del out
+            shutil.rmtree(os.path.join(base, "s"), ignore_errors=True)
+            best_s = max(best_s, nbytes / (t1 - t0) / 1e9)
+            best_r = max(best_r, nbytes / (t2 - t1) / 1e9)
+        native.release_pool()
+        print(json.dumps({"slot_MiB": slot >> 20, "slots": nslots, "threads": threads,
+                          "save_GBps": round(best_s, 2), "restore_GBps": round(best_r, 2),
+                          "bytes": nbytes}), flush=True)
+    shutil.rmtree(base, ignore_errors=True)
+
+
+if __name__ == "__main__":
+    main()
