@@ -524,7 +524,8 @@ def run_c5(args) -> dict:
             shutil.rmtree(os.path.join(base, "sync"), ignore_errors=True)
     sync_save_ms = sync_ms[-1]
     cycles = int(args.train_ms * 1.965e6)
-    ck = tv.Checkpointer(rt, "run", tv.RetentionPolicy(keep_last=3), tv.SaveOptions(sync=False))
+    ck = tv.Checkpointer(rt, "run", tv.RetentionPolicy(keep_last=3), tv.SaveOptions(sync=False),
+                         background_delete=not args.inline_gc)
     blocking, waits, joins, gcs, bg = [], [], [], [], []
     t_start = time.perf_counter()
     for step in range(args.steps):
@@ -561,7 +562,8 @@ def run_c5(args) -> dict:
         "config": {
             "workload": f"C5 Checkpointer(keep_last=3, async) every step over {args.steps} steps, "
                         f"Llama-3-8B {args.layers} layers ({tree_bytes} bytes) FSDP-{N}, synthetic "
-                        f"training step = {args.train_ms} ms GPU time + in-place param update",
+                        f"training step = {args.train_ms} ms GPU time + in-place param update, "
+                        f"retention deletes {'inline (reference)' if args.inline_gc else 'in the background'}",
             "config": "c5",
         },
         "blocking_ms_mean": round(statistics.mean(steady), 2),
@@ -810,6 +812,7 @@ def main() -> None:
     ap.add_argument("--restore-gpus", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--train-ms", type=float, default=1000.0)
+    ap.add_argument("--inline-gc", action="store_true", help="c5: retention deletes inside wait() (reference)")
     args = ap.parse_args()
     if args.impl == "reference":
         d = Dist()

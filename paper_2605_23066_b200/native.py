@@ -313,14 +313,16 @@ class Engine:
 
 
 class EngineConfig:
-    """Pipeline sizing.  Defaults: 32 × 8 MiB pinned slots (DDIO/L3-friendly pwrite
-    blocks, deep enough to keep PCIe busy while 16 threads write), device staging of the
-    same size, threads = host cores shared by the engines running at once."""
+    """Pipeline sizing.  Defaults: 32 × 2 MiB pinned slots — a ring small enough to stay
+    in the host's last-level cache (the DMA'd bytes are re-read by pwrite from cache),
+    deep enough to keep PCIe busy while every core writes; measured best in
+    profiles/r01_engine_sweep.jsonl.  Threads = host cores shared by the engines running
+    at once."""
 
     def __init__(self, slot_bytes: int | None = None, n_slots: int | None = None,
                  staging_bytes: int | None = None, threads: int | None = None):
         env = os.environ
-        self.slot_bytes = int(slot_bytes or env.get("TVGPU_SLOT_BYTES", 8 << 20))
+        self.slot_bytes = int(slot_bytes or env.get("TVGPU_SLOT_BYTES", 2 << 20))
         self.n_slots = int(n_slots or env.get("TVGPU_SLOTS", 32))
         self.staging_bytes = int(staging_bytes or env.get("TVGPU_STAGING_BYTES", 0)) or max(
             self.n_slots * self.slot_bytes, 1 << 30
