@@ -546,7 +546,7 @@ def run_c5(args) -> dict:
             if "finalized" in tl and "snapshotted" in tl:
                 bg.append((tl["finalized"] - tl["snapshotted"]) * 1e3)
         prev = handle
-    ck.wait()
+    ck.close()
     loop_s = time.perf_counter() - t_start
     kept = ck.all_steps()
     assert kept == list(range(args.steps - 3, args.steps)), kept

@@ -39,6 +39,21 @@ extern "C" {
 #define TV_ERR_NOMEM (-4)  /* pinned / device staging allocation failed          */
 #define TV_ERR_STATE (-5)  /* engine misuse (e.g. wrong device)                  */
 
+/* Element types of converting copies (tv_copy.src_dtype / dst_dtype). */
+#define TV_DT_RAW 0        /* no conversion: bytes are copied                     */
+#define TV_DT_F32 1
+#define TV_DT_F64 2
+#define TV_DT_I32 3
+#define TV_DT_I64 4
+#define TV_DT_U8 5
+#define TV_DT_BOOL 6
+#define TV_DT_BF16 7
+
+/* Bits a converting copy ORs into its flags word (treemodel.py:417-441 checks). */
+#define TV_CAST_OVERFLOW 1u     /* integer narrowing / float->int out of range         */
+#define TV_CAST_NONINTEGRAL 2u  /* float->int of a non-integral value                  */
+#define TV_CAST_NONFINITE 4u    /* float->int of inf / nan                              */
+
 /* A box inside one row-major array. */
 typedef struct tv_array_box {
   uint64_t base;                /* address of element (0,…,0) of the array           */
@@ -47,13 +62,19 @@ typedef struct tv_array_box {
 } tv_array_box;
 
 /* One N-d box copy src → dst (same extents).  Pack is dst = a dense box of shape ext,
- * unpack is src = a dense box; both sides may be strided (reshard scatter). */
+ * unpack is src = a dense box; both sides may be strided (reshard scatter).
+ * With src_dtype != TV_DT_RAW the copy converts element types on the fly (the load-time
+ * cast of treemodel.py:444-484 fused into the unpack): round-to-nearest-even float
+ * narrowing, checked integer narrowing; violations are OR-ed into *flags. */
 typedef struct tv_copy {
   tv_array_box src;
   tv_array_box dst;
   int64_t ext[TV_MAX_RANK];
   int32_t rank;                 /* 0 ≤ rank ≤ TV_MAX_RANK (rank 0 = one element)     */
-  int32_t itemsize;             /* bytes per element                                  */
+  int32_t itemsize;             /* bytes per (source) element                         */
+  int32_t src_dtype;            /* TV_DT_RAW, or the source TV_DT_* of a conversion   */
+  int32_t dst_dtype;            /* destination TV_DT_* of a conversion                */
+  uint64_t flags;               /* conversion: device address of a uint32 check word  */
 } tv_copy;
 
 /* One chunk payload to persist (save side).  The payload is the row-major bytes of

@@ -683,12 +683,17 @@ class ChunkReader:
 
 @dataclass
 class Destination:
-    """A target box on a GPU: the tensor at ``address`` holds global box ``ranges``."""
+    """A target box on a GPU: the tensor at ``address`` holds global box ``ranges``.
+    ``src_code``/``dst_code`` (native.DTYPE_CODE) make the copy into it converting (the
+    fused load-time cast); ``itemsize`` is then the destination element size."""
 
     gpu: int
     address: int
     ranges: tuple[Range, ...]
     itemsize: int
+    src_code: int = 0
+    dst_code: int = 0
+    src_itemsize: int = 0
 
 
 @dataclass
@@ -696,6 +701,7 @@ class FetchItem:
     fetch: Fetch
     reader_gpu: int
     consumers: list[Destination] = field(default_factory=list)
+    cast_flags: int = 0   # device address of the leaf's check word on the reader GPU
 
 
 def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurrent: int = 1):
@@ -752,13 +758,13 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     direct_dst = np.zeros(len(items), np.uint64)
     first_copy = np.zeros(len(items), np.int32)
     n_copies = np.zeros(len(items), np.int32)
-    cols: dict[str, list] = {k: [] for k in ("sb", "ss", "so", "db", "ds", "do", "ext", "isz")}
+    cols: dict[str, list] = {k: [] for k in ("sb", "ss", "so", "db", "ds", "do", "ext", "isz", "sdt", "ddt", "flg")}
     for j, it in enumerate(items):
         f = it.fetch
         fetched = tuple(zip(f.origin, f.shape))
         direct = None
         for d in it.consumers:
-            if d.gpu != it.reader_gpu:
+            if d.gpu != it.reader_gpu or d.src_code:
                 continue
             if not all(do <= fo and fo + fe <= do + de for (fo, fe), (do, de) in zip(fetched, d.ranges)):
                 continue
@@ -782,7 +788,10 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
             cols["ds"].append(tuple(e for _, e in d.ranges))
             cols["do"].append(tuple(h - o for (h, _), (o, _) in zip(hit, d.ranges)))
             cols["ext"].append(tuple(e for _, e in hit))
-            cols["isz"].append(d.itemsize)
+            cols["isz"].append(d.src_itemsize if d.src_code else d.itemsize)
+            cols["sdt"].append(d.src_code)
+            cols["ddt"].append(d.dst_code)
+            cols["flg"].append(it.cast_flags if d.src_code else 0)
         n_copies[j] = len(cols["ext"]) - first_copy[j]
     ritems["input"] = [input_index[it.fetch.key] for it in items]
     ritems["device"] = [it.reader_gpu for it in items]
@@ -792,7 +801,7 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     ritems["first_copy"] = first_copy
     ritems["n_copies"] = n_copies
     copies = native.copy_table(cols["sb"], cols["ss"], cols["so"], cols["db"], cols["ds"], cols["do"],
-                               cols["ext"], cols["isz"])
+                               cols["ext"], cols["isz"], cols["sdt"], cols["ddt"], cols["flg"])
     cfg = engine_cfg or native.EngineConfig()
     with native.engine_lease(cfg, concurrent) as eng:
         stats = eng.load(ritems, inputs, copies)

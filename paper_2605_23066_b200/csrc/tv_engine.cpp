@@ -157,9 +157,19 @@ class JobUploader {
   }
   // Copies `jobs`, launches the kernel, retires the region with an event.
   int run(std::vector<CopyJob>& jobs, cudaStream_t stream, int64_t* launches) {
+    return run_generic(jobs, stream, launches, plan_units, launch_copy_jobs);
+  }
+  int run_cast(std::vector<CastJob>& jobs, cudaStream_t stream, int64_t* launches) {
+    return run_generic(jobs, stream, launches, plan_cast_units, launch_cast_jobs);
+  }
+
+ private:
+  template <typename Job, typename Plan, typename Launch>
+  int run_generic(std::vector<Job>& jobs, cudaStream_t stream, int64_t* launches, Plan plan,
+                  Launch launch) {
     if (jobs.empty()) return TV_OK;
-    const int64_t total_units = plan_units(jobs);
-    const size_t bytes = jobs.size() * sizeof(CopyJob);
+    const int64_t total_units = plan(jobs);
+    const size_t bytes = jobs.size() * sizeof(Job);
     std::lock_guard<std::mutex> g(m_);
     if (bytes > cap_) {
       // Grow (rare): drain everything, reallocate.
@@ -190,8 +200,8 @@ class JobUploader {
     std::memcpy(host_ + head_, jobs.data(), bytes);
     TV_CUDA_CHECK(cudaMemcpyAsync(dev_ + head_, host_ + head_, bytes, cudaMemcpyHostToDevice,
                                   stream));
-    TV_CUDA_CHECK(launch_copy_jobs(reinterpret_cast<const CopyJob*>(dev_ + head_),
-                                   (int)jobs.size(), total_units, stream));
+    TV_CUDA_CHECK(launch(reinterpret_cast<const Job*>(dev_ + head_), (int)jobs.size(), total_units,
+                         stream));
     cudaEvent_t ev;
     if (free_events_.empty()) {
       TV_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -206,7 +216,6 @@ class JobUploader {
     return TV_OK;
   }
 
- private:
   struct Region {
     size_t off, len;
     cudaEvent_t ev;
@@ -1041,11 +1050,13 @@ class LoadRun {
     cudaSetDevice(it.device);
     if (it.n_copies > 0) {
       std::vector<CopyJob> jobs;
+      std::vector<CastJob> casts;
       std::string why;
       for (int c = 0; c < it.n_copies; ++c) {
         tv_copy cp = copies_[it.first_copy + c];
         cp.src.base = reinterpret_cast<uint64_t>(st.base) + cp.src.base;
-        if (!normalize(cp, jobs, why)) {
+        const bool ok = is_cast(cp) ? normalize_cast(cp, casts, why) : normalize(cp, jobs, why);
+        if (!ok) {
           err_.set(TV_ERR_ARG, "unpack: " + why);
           return;
         }
@@ -1053,6 +1064,7 @@ class LoadRun {
       }
       int64_t launches = 0;
       int rc = ctx->uploader->run(jobs, ctx->stream, &launches);
+      if (rc == TV_OK) rc = ctx->uploader->run_cast(casts, ctx->stream, &launches);
       if (rc != TV_OK) {
         err_.set(rc, get_error());
         return;
@@ -1155,14 +1167,17 @@ int engine_load(tv_engine* e, const tv_read_item* items, int n_items, const tv_i
 // Standalone batched copy (tv_copy_boxes): one launch on the caller's stream.
 int copy_boxes(int device, const tv_copy* copies, int n, cudaStream_t stream) {
   std::vector<CopyJob> jobs;
+  std::vector<CastJob> casts;
   std::string why;
   for (int i = 0; i < n; ++i) {
-    if (!normalize(copies[i], jobs, why)) {
+    const bool ok = is_cast(copies[i]) ? normalize_cast(copies[i], casts, why)
+                                       : normalize(copies[i], jobs, why);
+    if (!ok) {
       set_error("tv_copy_boxes: copy " + std::to_string(i) + ": " + why);
       return TV_ERR_ARG;
     }
   }
-  if (jobs.empty()) return TV_OK;
+  if (jobs.empty() && casts.empty()) return TV_OK;
   static std::mutex m;
   static std::map<int, std::unique_ptr<JobUploader>> uploaders;
   JobUploader* up;
@@ -1173,7 +1188,9 @@ int copy_boxes(int device, const tv_copy* copies, int n, cudaStream_t stream) {
     up = slot.get();
   }
   TV_CUDA_CHECK(cudaSetDevice(device));
-  return up->run(jobs, stream, nullptr);
+  int rc = up->run(jobs, stream, nullptr);
+  if (rc == TV_OK) rc = up->run_cast(casts, stream, nullptr);
+  return rc;
 }
 
 }  // namespace tv

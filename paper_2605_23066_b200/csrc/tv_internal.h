@@ -51,6 +51,32 @@ int64_t plan_units(std::vector<CopyJob>& jobs);
 cudaError_t launch_copy_jobs(const CopyJob* dev_jobs, int n_jobs, int64_t total_units,
                              cudaStream_t stream);
 
+// Converting copy (load-time cast fused into the unpack): like CopyJob but in elements,
+// with different element sizes on both sides.
+struct CastJob {
+  const char* src;
+  char* dst;
+  int64_t run;        // elements per contiguous run
+  int64_t n[3];
+  int64_t ss[3];      // source byte strides of the outer dims
+  int64_t ds[3];      // destination byte strides
+  int64_t nruns;
+  int64_t units;
+  int64_t unit_begin;
+  uint32_t* flags;    // check word (TV_CAST_* bits)
+  int32_t sdt;        // TV_DT_* source / destination element types
+  int32_t ddt;
+  int32_t mode;       // 0 = warp per run segment, 1 = flat (short runs)
+  int32_t pad;
+};
+
+bool is_cast(const tv_copy& c);
+int dtype_size(int dt);
+bool normalize_cast(const tv_copy& c, std::vector<CastJob>& out, std::string& err);
+int64_t plan_cast_units(std::vector<CastJob>& jobs);
+cudaError_t launch_cast_jobs(const CastJob* dev_jobs, int n_jobs, int64_t total_units,
+                             cudaStream_t stream);
+
 // Is the box a single contiguous byte range of its array?  Sets byte offset/length.
 bool box_contiguous(const tv_array_box& b, const int64_t* ext, int rank, int itemsize,
                     int64_t* byte_off, int64_t* nbytes);

@@ -34,9 +34,13 @@ ARRAY_BOX = np.dtype(
 )
 COPY = np.dtype(
     [("src", ARRAY_BOX), ("dst", ARRAY_BOX), ("ext", "<i8", (MAX_RANK,)), ("rank", "<i4"),
-     ("itemsize", "<i4")],
+     ("itemsize", "<i4"), ("src_dtype", "<i4"), ("dst_dtype", "<i4"), ("flags", "<u8")],
     align=True,
 )
+
+# element type codes of converting copies (include/tvgpu.h TV_DT_*)
+DTYPE_CODE = {"f32": 1, "f64": 2, "i32": 3, "i64": 4, "u8": 5, "bool": 6, "bf16": 7}
+CAST_OVERFLOW, CAST_NONINTEGRAL, CAST_NONFINITE = 1, 2, 4
 WRITE_ITEM = np.dtype(
     [("src", ARRAY_BOX), ("ext", "<i8", (MAX_RANK,)), ("rank", "<i4"), ("itemsize", "<i4"),
      ("file", "<i4"), ("device", "<i4"), ("file_off", "<i8")],
@@ -148,8 +152,10 @@ def pad_rows(rows: Sequence[Sequence[int]]) -> np.ndarray:
     return out
 
 
-def copy_table(src_base, src_shape, src_off, dst_base, dst_shape, dst_off, ext, itemsize) -> np.ndarray:
-    """COPY table from per-copy lists (bases ints, shapes/offsets/extents tuples)."""
+def copy_table(src_base, src_shape, src_off, dst_base, dst_shape, dst_off, ext, itemsize,
+               src_dtype=None, dst_dtype=None, flags=None) -> np.ndarray:
+    """COPY table from per-copy lists (bases ints, shapes/offsets/extents tuples); the
+    optional dtype-code / flag-address columns turn rows into converting copies."""
     n = len(ext)
     t = np.zeros(n, COPY)
     if n == 0:
@@ -163,6 +169,10 @@ def copy_table(src_base, src_shape, src_off, dst_base, dst_shape, dst_off, ext, 
     t["ext"] = pad_rows(ext)
     t["rank"] = [len(e) for e in ext]
     t["itemsize"] = itemsize
+    if src_dtype is not None:
+        t["src_dtype"] = src_dtype
+        t["dst_dtype"] = dst_dtype
+        t["flags"] = np.asarray(flags, np.uint64)
     return t
 
 

@@ -223,3 +223,55 @@ def target_spec(c: dict, load: dict, path: str, leaf) -> tuple | None:
     if ndim == 0:
         return None
     return (mesh["axes"], mesh["P"], mesh["replica_axis"], (mesh["axis"],) + (None,) * (ndim - 1))
+
+
+# -- load-time casts ----------------------------------------------------------------------
+
+CAST_DTYPES = ["f32", "f64", "i32", "i64", "u8"]
+
+
+def cast_input(src: str, dst: str, kind: str, seed: int = 0) -> np.ndarray:
+    """Deterministic (64, 48) input for a cast src -> dst.  kind "ok" is castable by the
+    reference; "overflow" / "nonfinite" / "nonintegral" trigger its checks."""
+    rng = np.random.default_rng(7000 + seed + 31 * CAST_DTYPES.index(src) + CAST_DTYPES.index(dst))
+    shape = (64, 48)
+    int_dst = dst in ("i32", "i64", "u8")
+    if src in ("f32", "f64"):
+        if int_dst:
+            lo, hi = (0, 255) if dst == "u8" else (-2**20, 2**20)
+            x = rng.integers(lo, hi, shape).astype(NP[src])
+            if kind == "overflow":
+                x[3, 5] = 1e12 if dst != "i64" else 1e19
+            elif kind == "nonfinite":
+                x[7, 1] = np.inf
+            elif kind == "nonintegral":
+                x[2, 2] += 0.5
+        else:
+            x = (rng.standard_normal(shape) * 1e3).astype(NP[src])
+            x[0, :4] = [1.0000001, -2.5e-39, 3.4e38, 65504.123]
+    else:
+        if int_dst:
+            lo, hi = {"u8": (0, 256), "i32": (-2**31, 2**31), "i64": (-2**62, 2**62)}[src]
+            dlo, dhi = {"u8": (0, 256), "i32": (-2**31, 2**31), "i64": (-2**62, 2**62)}[dst]
+            x = rng.integers(max(lo, dlo), min(hi, dhi), shape).astype(NP[src])
+            if kind == "overflow":
+                x[4, 4] = hi - 1 if hi > dhi else lo
+        else:
+            lo, hi = {"u8": (0, 256), "i32": (-2**31, 2**31), "i64": (-2**62, 2**62)}[src]
+            x = rng.integers(lo, hi, shape).astype(NP[src])
+    return np.ascontiguousarray(x)
+
+
+def cast_cases() -> list[tuple[str, str, str]]:
+    out = []
+    for s in CAST_DTYPES:
+        for d in CAST_DTYPES:
+            if s == d:
+                continue
+            out.append((s, d, "ok"))
+            if d in ("i32", "i64", "u8"):
+                if s in ("f32", "f64"):
+                    out += [(s, d, "overflow"), (s, d, "nonfinite"), (s, d, "nonintegral")]
+                elif (s, d) in (("i64", "i32"), ("i64", "u8"), ("i32", "u8")):
+                    out.append((s, d, "overflow"))
+    return out

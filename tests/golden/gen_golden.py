@@ -168,8 +168,25 @@ def run_load(tv, c, load, backend, tree, arrays, shardings) -> dict:
     return {"load": load, "process_count": P, "counters": counters, "arrays": digests}
 
 
+def cast_fixture(tv) -> dict:
+    """The reference's cast_leaf (treemodel.py:444-484) on every numeric dtype pair."""
+    out = []
+    for src, dst, kind in cases.cast_cases():
+        x = cases.cast_input(src, dst, kind)
+        rec = {"src": src, "dst": dst, "kind": kind}
+        try:
+            got = tv.cast_leaf(tv.DenseArray(src, x), tv.AbstractLeaf("array", x.shape, dst))
+            rec["sha256"] = sha(got.data.tobytes())
+        except tv.TreevaultError as exc:
+            rec["error"] = type(exc).__name__
+            rec["message"] = str(exc)
+        out.append(rec)
+    return {"casts": out}
+
+
 def main() -> None:
     tv = _import_reference()
+    (HERE / "casts.json").write_text(json.dumps(cast_fixture(tv), indent=1, sort_keys=True))
     for c in cases.CASES:
         fixture = run_case(tv, c)
         (HERE / f"{c['name']}.json").write_text(json.dumps(fixture, indent=1, sort_keys=True))

@@ -10,6 +10,7 @@ int main(void) {
   F(tv_array_box, base); F(tv_array_box, shape); F(tv_array_box, off);
   printf("tv_copy %zu\n", sizeof(tv_copy));
   F(tv_copy, src); F(tv_copy, dst); F(tv_copy, ext); F(tv_copy, rank); F(tv_copy, itemsize);
+  F(tv_copy, src_dtype); F(tv_copy, dst_dtype); F(tv_copy, flags);
   printf("tv_write_item %zu\n", sizeof(tv_write_item));
   F(tv_write_item, src); F(tv_write_item, ext); F(tv_write_item, rank); F(tv_write_item, itemsize);
   F(tv_write_item, file); F(tv_write_item, device); F(tv_write_item, file_off);
