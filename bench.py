@@ -400,6 +400,17 @@ def run_ours(args) -> dict:
     clock_info = clocks.stop() if d.rank == 0 else {}
     kernels = d.sum(after["kernel_launches"] - before["kernel_launches"])
     dmas = d.sum(after["dma_copies"] - before["dma_copies"])
+    engine = {}
+    for kind in ("save", "load"):
+        a, b = after[kind], before[kind]
+        wall = max(1e-9, a["seconds_total"] - b["seconds_total"])
+        engine[kind] = {
+            "wall_s": round(wall, 3),
+            "thread_io_s": round(a["seconds_io"] - b["seconds_io"], 3),
+            "thread_wait_dma_s": round(a["seconds_wait_dma"] - b["seconds_wait_dma"], 3),
+            "producer_wait_slot_s": round(a["seconds_wait_slot"] - b["seconds_wait_slot"], 3),
+            "storage_GB": round((a["bytes_storage"] - b["bytes_storage"]) / 1e9, 3),
+        }
     save_ms = statistics.mean(saves)
     restore_ms = statistics.mean(restores)
     step_ms = save_ms + restore_ms
@@ -467,6 +478,7 @@ def run_ours(args) -> dict:
                     "strided boxes, snapshots and reshard scatters run box_copy_kernel",
         },
         "clocks": clock_info,
+        "engine_rank0": engine,
     }
     if d.rank == 0:
         pcie_d2h = probe["pcie_d2h_GBps_per_gpu"] * N

@@ -131,6 +131,9 @@ typedef struct tv_stats {
   int64_t files;                /* files committed (save) or opened (restore)         */
   double seconds_total;
   double seconds_kernel;        /* CUDA-event time of box-copy kernels                */
+  double seconds_io;            /* storage threads: time inside pwrite/pread (summed) */
+  double seconds_wait_dma;      /* storage threads: time waiting for D2H/H2D events   */
+  double seconds_wait_slot;     /* producer: time waiting for a free pinned slot      */
 } tv_stats;
 
 typedef struct tv_engine tv_engine;

@@ -52,6 +52,13 @@ double now_s() {
       .count();
 }
 
+// Accumulates seconds from many threads.
+struct Clock {
+  std::atomic<int64_t> ns{0};
+  void add(double seconds) { ns += (int64_t)(seconds * 1e9); }
+  double seconds() const { return ns.load() * 1e-9; }
+};
+
 std::string errno_msg(const std::string& what, const std::string& path) {
   return what + " " + path + ": " + std::strerror(errno);
 }
@@ -527,6 +534,8 @@ class SaveRun {
     const int L = std::max(1, e_->n_threads);
     lanes_.clear();
     for (int k = 0; k < L; ++k) lanes_.emplace_back(new Queue<SaveSlot>());
+    inflight_.reset(new std::atomic<int>[L]);
+    for (int k = 0; k < L; ++k) inflight_[k] = 0;
     cursors_.assign(L, LaneCursor());
     std::vector<int> order(n_outs_);
     for (int o = 0; o < n_outs_; ++o) order[o] = o;
@@ -609,17 +618,30 @@ class SaveRun {
     std::vector<int> active;
     for (size_t k = 0; k < cursors_.size(); ++k)
       if (!cursors_[k].finished()) active.push_back((int)k);
+    // A lane never holds more than its share of the ring, so a slow writer cannot starve
+    // the others of slots.
+    const int cap = std::max(2, (int)(2 * e_->n_slots / std::max<size_t>(1, active.size())));
     while (!active.empty() && !err_.failed.load()) {
       std::vector<int> still;
+      bool progressed = false;
       for (int k : active) {
         if (err_.failed.load()) return;
+        if (inflight_[k].load() >= cap) {
+          still.push_back(k);
+          continue;
+        }
+        progressed = true;
         int s;
+        const double t0 = now_s();
         if (!free_slots_.pop(s)) return;
+        wait_slot_.add(now_s() - t0);
+        inflight_[k]++;
         SaveSlot cur;
         cur.index = s;
         cur.lane = k;
         if (!fill_slot(cursors_[k], cur)) return;
         if (cur.fill == 0 && cur.writes.empty()) {
+          inflight_[k]--;
           free_slots_.push(s);
         } else if (!submit(cur)) {
           return;
@@ -627,6 +649,7 @@ class SaveRun {
         if (!cursors_[k].finished()) still.push_back(k);
       }
       active.swap(still);
+      if (!progressed) std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
   }
 
@@ -706,15 +729,20 @@ class SaveRun {
     SaveSlot s;
     while (lanes_[lane]->pop(s)) {
       if (!err_.failed.load()) {
+        const double t0 = now_s();
         cudaError_t ce = cudaEventSynchronize(s.ev);
+        wait_dma_.add(now_s() - t0);
         if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("D2H/pack: ") + cudaGetErrorString(ce));
       }
       if (!err_.failed.load()) {
         const char* host = e_->slots[s.index];
+        const double t0 = now_s();
         for (auto& w : s.writes) {
           if (!write_seg(w, host)) break;
         }
+        io_.add(now_s() - t0);
       }
+      inflight_[lane]--;
       free_slots_.push(s.index);
     }
   }
@@ -805,6 +833,9 @@ class SaveRun {
     stats_->kernel_launches += stats_launches_.load();
     stats_->dma_copies += stats_dma_.load();
     stats_->files += files_.load();
+    stats_->seconds_io += io_.seconds();
+    stats_->seconds_wait_dma += wait_dma_.seconds();
+    stats_->seconds_wait_slot += wait_slot_.seconds();
   }
 
  private:
@@ -816,7 +847,9 @@ class SaveRun {
   std::unique_ptr<OutputState[]> outs_;
   Queue<int> free_slots_;
   std::vector<std::unique_ptr<Queue<SaveSlot>>> lanes_;
+  std::unique_ptr<std::atomic<int>[]> inflight_;
   std::vector<LaneCursor> cursors_;
+  Clock io_, wait_dma_, wait_slot_;
   std::vector<int> lane_of_;
   ErrorSlot err_;
   DirMaker dirs_;
@@ -915,6 +948,9 @@ class LoadRun {
     stats_->kernel_launches += launches_.load();
     stats_->dma_copies += dma_.load();
     stats_->files += files_.load();
+    stats_->seconds_io += io_.seconds();
+    stats_->seconds_wait_dma += wait_dma_.seconds();
+    stats_->seconds_wait_slot += wait_slot_.seconds();
   }
 
  private:
@@ -934,11 +970,15 @@ class LoadRun {
 
   int acquire_slot() {
     int s;
+    const double t0 = now_s();
     if (!free_slots_.pop(s)) return -1;
+    const double t1 = now_s();
+    wait_slot_.add(t1 - t0);
     if (slot_events_[s]) {
       cudaSetDevice(slot_event_dev_[s]);
       cudaEventSynchronize(slot_events_[s]);  // previous H2D out of this slot done
     }
+    wait_dma_.add(now_s() - t1);
     return s;
   }
 
@@ -1015,7 +1055,9 @@ class LoadRun {
     const auto& it = items_[t.item];
     ItemState& st = states_[t.item];
     char* host = e_->slots[t.slot];
+    const double t0 = now_s();
     if (!fetch(ins_[it.input], host, it.in_off + t.off, t.n)) return false;
+    io_.add(now_s() - t0);
     bytes_storage_ += t.n;
     DeviceCtx* ctx = ctx_for(it.device);
     if (!ctx) return false;
@@ -1097,6 +1139,7 @@ class LoadRun {
   std::map<int, DeviceCtx*> used_devices_;
   std::atomic<int64_t> bytes_device_{0}, bytes_storage_{0}, bytes_packed_{0}, launches_{0},
       dma_{0}, files_{0};
+  Clock io_, wait_dma_, wait_slot_;
 };
 
 }  // namespace

@@ -56,7 +56,8 @@ INPUT = OUTPUT
 STATS = np.dtype(
     [("bytes_device", "<i8"), ("bytes_storage", "<i8"), ("bytes_packed", "<i8"),
      ("kernel_launches", "<i8"), ("dma_copies", "<i8"), ("files", "<i8"),
-     ("seconds_total", "<f8"), ("seconds_kernel", "<f8")],
+     ("seconds_total", "<f8"), ("seconds_kernel", "<f8"), ("seconds_io", "<f8"),
+     ("seconds_wait_dma", "<f8"), ("seconds_wait_slot", "<f8")],
     align=True,
 )
 
@@ -198,20 +199,27 @@ def write_table(src_base, src_shape, src_off, ext, itemsize, file, device, file_
 
 # Process-wide counters of native work (bench.py reports the kernel launches and DMA
 # transfers its timed region issued).
-TOTALS = {"kernel_launches": 0, "dma_copies": 0, "bytes_device": 0, "bytes_storage": 0,
-          "bytes_packed": 0, "files": 0}
+_FIELDS = ("kernel_launches", "dma_copies", "bytes_device", "bytes_storage", "bytes_packed", "files",
+           "seconds_total", "seconds_io", "seconds_wait_dma", "seconds_wait_slot")
+TOTALS = {"save": dict.fromkeys(_FIELDS, 0), "load": dict.fromkeys(_FIELDS, 0),
+          "kernels": {"kernel_launches": 0}}
 _totals_lock = threading.Lock()
 
 
-def _account(stats) -> None:
+def _account(kind: str, stats) -> None:
     with _totals_lock:
-        for k in TOTALS:
-            TOTALS[k] += int(stats[k])
+        for k in _FIELDS:
+            TOTALS[kind][k] += stats[k].item()
 
 
 def totals() -> dict:
+    """Combined counters plus the per-kind ("save" / "load") breakdown."""
     with _totals_lock:
-        return dict(TOTALS)
+        out = {k: TOTALS["save"][k] + TOTALS["load"][k] for k in _FIELDS}
+        out["kernel_launches"] += TOTALS["kernels"]["kernel_launches"]
+        out["save"] = dict(TOTALS["save"])
+        out["load"] = dict(TOTALS["load"])
+        return out
 
 
 def copy_boxes(device: int, copies: np.ndarray, stream: int = 0) -> None:
@@ -221,7 +229,7 @@ def copy_boxes(device: int, copies: np.ndarray, stream: int = 0) -> None:
         return
     check(lib().tv_copy_boxes(device, _ptr(copies), len(copies), stream), "tv_copy_boxes")
     with _totals_lock:
-        TOTALS["kernel_launches"] += 1
+        TOTALS["kernels"]["kernel_launches"] += 1
 
 
 def enable_peer_access(gpus: Sequence[int]) -> None:
@@ -306,7 +314,7 @@ class Engine:
         outputs = np.ascontiguousarray(outputs, OUTPUT)
         rc = lib().tv_engine_save(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
                                   stats.ctypes.data)
-        _account(stats[0])
+        _account("save", stats[0])
         check(rc, "tv_engine_save")
         return stats[0]
 
@@ -317,7 +325,7 @@ class Engine:
         copies = np.ascontiguousarray(copies, COPY)
         rc = lib().tv_engine_load(self._h, _ptr(items), len(items), _ptr(inputs), len(inputs),
                                   _ptr(copies), len(copies), stats.ctypes.data)
-        _account(stats[0])
+        _account("load", stats[0])
         check(rc, "tv_engine_load")
         return stats[0]
 

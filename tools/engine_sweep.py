@@ -61,8 +61,7 @@ def main():
             if rep > 0:  # rep 0 warms every setting up
                 best_s = max(best_s, nbytes / (t1 - t0) / 1e9)
                 best_r = max(best_r, nbytes / (t2 - t1) / 1e9)
-        results[(slot, nslots, threads)] = (best_s, best_r)
-        native.release_pool()
+        results[(slot, nslots, threads)] = (best_s, best_r)  # engines stay pooled (no re-pinning)
     for (slot, nslots, threads), (best_s, best_r) in results.items():
         print(json.dumps({"slot_MiB": slot / (1 << 20), "slots": nslots, "threads": threads,
                           "save_GBps": round(best_s, 2), "restore_GBps": round(best_r, 2),
