@@ -25,8 +25,10 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--dir", default="/dev/shm/tvsweep")
+    ap.add_argument("--settings", default=None, help="slotMiB:count,... e.g. 2:32,8:32")
     args = ap.parse_args()
-    base = "/dev/shm/tvsweep"
+    base = args.dir
     shutil.rmtree(base, ignore_errors=True)
     backend = tv.FilesystemBackend(base)
     rt = tv.SimulatedRuntime(1, backend, gpus=[0])
@@ -39,6 +41,9 @@ def main():
                 (4 << 20, 32, cores), (4 << 20, 64, cores), (1 << 20, 128, cores)]
     if args.quick:
         settings += [(4 << 20, 16, cores), (16 << 20, 16, cores), (8 << 20, 32, cores // 2)]
+    if args.settings:
+        settings = [(int(float(a) * (1 << 20)), int(b), cores)
+                    for a, b in (x.split(":") for x in args.settings.split(","))]
     i = 0
     results = {}
     # interleave settings across repetitions so slow drift of the box hits all of them
