@@ -330,30 +330,70 @@ class Engine:
         return stats[0]
 
 
+def _llc_bytes() -> int:
+    """Total last-level cache of the host (sum over distinct L3 instances), 0 if unknown."""
+    import glob
+
+    seen, total = set(), 0
+    for path in glob.glob("/sys/devices/system/cpu/cpu*/cache/index3"):
+        try:
+            with open(f"{path}/shared_cpu_list") as f:
+                key = f.read().strip()
+            if key in seen:
+                continue
+            seen.add(key)
+            with open(f"{path}/size") as f:
+                txt = f.read().strip().upper()
+            mult = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}.get(txt[-1], 1)
+            total += int(txt.rstrip("KMG")) * mult
+        except OSError:
+            continue
+    return total
+
+
+def _host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 8)
+
+
 class EngineConfig:
-    """Pipeline sizing.  Defaults: 32 × 2 MiB pinned slots — a ring small enough to stay
-    in the host's last-level cache (the DMA'd bytes are re-read by pwrite from cache),
-    deep enough to keep PCIe busy while every core writes; measured best in
-    profiles/r01_engine_sweep.jsonl.  Threads = host cores shared by the engines running
-    at once."""
+    """Pipeline sizing.
+
+    threads  — host cores shared by the engines running at once on this box (the
+               threads runtime's processes, or torchrun's LOCAL_WORLD_SIZE ranks);
+    n_slots  — 2 pinned slots per storage thread (fewer starves the readers);
+    slot     — 2 MiB, or 1 MiB when the rings of all engines would not fit the host's
+               last-level cache: the DMA'd bytes are re-read by pwrite / the H2D straight
+               from the LLC (DDIO).  Measured best on these boxes
+               (profiles/r01_engine_sweep_*.jsonl).
+    """
 
     def __init__(self, slot_bytes: int | None = None, n_slots: int | None = None,
                  staging_bytes: int | None = None, threads: int | None = None):
         env = os.environ
-        self.slot_bytes = int(slot_bytes or env.get("TVGPU_SLOT_BYTES", 2 << 20))
-        self.n_slots = int(n_slots or env.get("TVGPU_SLOTS", 32))
-        self.staging_bytes = int(staging_bytes or env.get("TVGPU_STAGING_BYTES", 0)) or max(
-            self.n_slots * self.slot_bytes, 1 << 30
-        )
+        self._slot_bytes = slot_bytes or (int(env["TVGPU_SLOT_BYTES"]) if "TVGPU_SLOT_BYTES" in env else None)
+        self._n_slots = n_slots or (int(env["TVGPU_SLOTS"]) if "TVGPU_SLOTS" in env else None)
+        self._staging = staging_bytes or (int(env["TVGPU_STAGING_BYTES"]) if "TVGPU_STAGING_BYTES" in env else None)
         self.threads = threads or (int(env["TVGPU_THREADS"]) if "TVGPU_THREADS" in env else None)
+
+    def _engines(self, concurrent: int) -> int:
+        return max(concurrent, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
 
     def threads_for(self, concurrent: int) -> int:
         if self.threads:
             return self.threads
-        # engines of other ranks on this box (torchrun) share the host cores too
-        concurrent = max(concurrent, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
-        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-        return max(2, (cores or 8) // max(1, concurrent))
+        return max(2, _host_cores() // self._engines(concurrent))
+
+    def sizing(self, concurrent: int) -> tuple[int, int, int, int]:
+        """(n_slots, slot_bytes, staging_bytes, threads) for an engine of this box."""
+        threads = self.threads_for(concurrent)
+        n_slots = self._n_slots or max(16, 2 * threads)
+        slot = self._slot_bytes
+        if slot is None:
+            llc = _llc_bytes()
+            ring_all = (2 << 20) * n_slots * self._engines(concurrent)
+            slot = (2 << 20) if (llc == 0 or ring_all <= 1.25 * llc) else (1 << 20)
+        staging = self._staging or max(n_slots * slot, 1 << 30)
+        return n_slots, slot, staging, threads
 
 
 _pool: dict[tuple, list[Engine]] = {}
@@ -364,7 +404,7 @@ class engine_lease:
     """Context manager borrowing an idle engine of the given sizing from the pool."""
 
     def __init__(self, cfg: EngineConfig, concurrent: int):
-        self.key = (cfg.n_slots, cfg.slot_bytes, cfg.staging_bytes, cfg.threads_for(concurrent))
+        self.key = cfg.sizing(concurrent)
         self.engine: Engine | None = None
 
     def __enter__(self) -> Engine:
