@@ -624,10 +624,7 @@ def run_c5(args) -> dict:
 def kernel_roofline(tv, native, state, rt, d) -> dict:
     """The box-copy kernel as the device snapshot of an async save: every local shard
     packed into one arena, ONE launch per GPU; algorithmic bytes = 2 × bytes copied."""
-    import numpy as np
     import torch
-
-    from paper_2605_23066_b200 import chunkstore
 
     regions = []
     for tree in state.values():

@@ -47,6 +47,7 @@ int tv_last_error(char* buf, size_t len) {
 }
 
 int tv_copy_boxes(int device, const tv_copy* copies, int n, void* stream) {
+  tv::DeviceGuard guard;
   if (n < 0 || (n > 0 && !copies)) {
     tv::set_error("tv_copy_boxes: bad arguments");
     return TV_ERR_ARG;
@@ -66,6 +67,7 @@ int64_t tv_copy_bytes(const tv_copy* copies, int n) {
 
 int tv_engine_create(int n_slots, int64_t slot_bytes, int64_t staging_bytes, int n_threads,
                      tv_engine** out) {
+  tv::DeviceGuard guard;
   if (!out) {
     tv::set_error("tv_engine_create: out is NULL");
     return TV_ERR_ARG;
@@ -73,10 +75,12 @@ int tv_engine_create(int n_slots, int64_t slot_bytes, int64_t staging_bytes, int
   return tv::engine_create(n_slots, slot_bytes, staging_bytes, n_threads, out);
 }
 
-int tv_engine_destroy(tv_engine* e) { return tv::engine_destroy(e); }
+int tv_engine_destroy(tv_engine* e) {
+  tv::DeviceGuard guard; return tv::engine_destroy(e); }
 
 int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
                    const tv_output* outputs, int n_outputs, tv_stats* stats) {
+  tv::DeviceGuard guard;
   if (!e || n_items < 0 || n_outputs < 0) {
     tv::set_error("tv_engine_save: bad arguments");
     return TV_ERR_ARG;
@@ -86,6 +90,7 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
 
 int tv_engine_load(tv_engine* e, const tv_read_item* items, int n_items, const tv_input* inputs,
                    int n_inputs, const tv_copy* copies, int n_copies, tv_stats* stats) {
+  tv::DeviceGuard guard;
   if (!e || n_items < 0 || n_inputs < 0 || n_copies < 0) {
     tv::set_error("tv_engine_load: bad arguments");
     return TV_ERR_ARG;
@@ -94,6 +99,7 @@ int tv_engine_load(tv_engine* e, const tv_read_item* items, int n_items, const t
 }
 
 int tv_enable_peer_access(const int* devices, int n) {
+  tv::DeviceGuard guard;
   for (int i = 0; i < n; ++i) {
     TV_CUDA_CHECK(cudaSetDevice(devices[i]));
     for (int j = 0; j < n; ++j) {
@@ -121,6 +127,7 @@ int tv_enable_peer_access(const int* devices, int n) {
 typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 int tv_ipc_export(int device, uint64_t ptr, uint8_t handle_out[64], uint64_t* base_offset_out) {
+  tv::DeviceGuard guard;
   TV_CUDA_CHECK(cudaSetDevice(device));
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -144,6 +151,7 @@ int tv_ipc_export(int device, uint64_t ptr, uint8_t handle_out[64], uint64_t* ba
 }
 
 int tv_ipc_import(int device, const uint8_t handle[64], uint64_t* ptr_out) {
+  tv::DeviceGuard guard;
   TV_CUDA_CHECK(cudaSetDevice(device));
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, 64);
@@ -154,6 +162,7 @@ int tv_ipc_import(int device, const uint8_t handle[64], uint64_t* ptr_out) {
 }
 
 int tv_ipc_close(int device, uint64_t ptr) {
+  tv::DeviceGuard guard;
   TV_CUDA_CHECK(cudaSetDevice(device));
   TV_CUDA_CHECK(cudaIpcCloseMemHandle(reinterpret_cast<void*>(ptr)));
   return TV_OK;
@@ -224,6 +233,7 @@ int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t
 }
 
 int tv_probe_pcie(int device, int64_t bytes, int reps, double* d2h_gbps, double* h2d_gbps) {
+  tv::DeviceGuard guard;
   TV_CUDA_CHECK(cudaSetDevice(device));
   char *d = nullptr, *h = nullptr;
   TV_CUDA_CHECK(cudaMalloc(&d, bytes));

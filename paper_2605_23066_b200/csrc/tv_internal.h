@@ -11,6 +11,18 @@
 
 namespace tv {
 
+// Restores the calling thread's current CUDA device on scope exit: no entry point of the
+// library may leave the caller (e.g. torch) on another device.
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // Thread-local last error (tv_last_error).
 void set_error(const std::string& msg);
 const std::string& get_error();

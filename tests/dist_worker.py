@@ -74,14 +74,18 @@ def datapath(base: str) -> None:
     rng = np.random.default_rng(3)
     tree = {"state": cases.llama_like(rng, layers=1, d=32, ffn=48, vocab=40, kv=8)}
     specs = {"state": cases.fsdp_shardings(tree["state"], [("fsdp", world)], world)}
+    # one unsharded leaf: process 0 writes it; on restore every rank receives a copy
+    tree["state"]["extra"] = {"bias": cases.arr(rng, "f64", (6, 5))}
     leaves = dict(cases.leaf_paths(tree["state"]))
     shardings, state = {}, {}
-    for path, spec in specs["state"].items():
-        axes, P, ra, entries = spec
-        mesh = tv.Mesh.create(list(axes), process_count=P, replica_axis=ra)
-        leaf = leaves[path]
-        s = tv.Sharding(mesh, tv.PartitionSpec(tuple(entries)), leaf[2].shape)
-        shardings[path] = s
+    for path, leaf in leaves.items():
+        spec = specs["state"].get(path)
+        s = None
+        if spec is not None:
+            axes, P, ra, entries = spec
+            mesh = tv.Mesh.create(list(axes), process_count=P, replica_axis=ra)
+            s = tv.Sharding(mesh, tv.PartitionSpec(tuple(entries)), leaf[2].shape)
+            shardings[path] = s
         node = state
         parts = path.split("/")
         for p in parts[:-1]:
@@ -103,7 +107,8 @@ def datapath(base: str) -> None:
     mesh2 = tv.Mesh.create([("replica", world), ("fsdp", 1)], process_count=world, replica_axis="replica")
     abstract = {}
     for path, leaf in leaves.items():
-        s2 = tv.Sharding(mesh2, tv.PartitionSpec(("fsdp",) + (None,) * (leaf[2].ndim - 1)), leaf[2].shape)
+        s2 = None if path.startswith("extra/") else tv.Sharding(
+            mesh2, tv.PartitionSpec(("fsdp",) + (None,) * (leaf[2].ndim - 1)), leaf[2].shape)
         node = abstract
         parts = path.split("/")
         for p in parts[:-1]:
@@ -119,6 +124,10 @@ def datapath(base: str) -> None:
         node = out["state"]
         for p in path.split("/"):
             node = node[p]
+        if path.startswith("extra/"):  # unsharded: a full copy on this rank's GPU
+            assert isinstance(node, tv.DenseArray) and node.on_device
+            assert node.tobytes() == leaf[2].tobytes(), path
+            continue
         assert sorted(node.shards) == [rt.rank], node.shards.keys()
         got = tv.DenseArray(leaf[1], node.shards[rt.rank]).tobytes()
         assert got == leaf[2].tobytes(), path

@@ -112,7 +112,7 @@ def run(case, layers, reps, fsdp=8):
         copies, moved, keep = make_fanout(layers)
     else:
         copies, moved, keep = make_case(case, layers, fsdp)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.current_stream(0)
     for _ in range(3):
         native.copy_boxes(0, copies, stream.cuda_stream)
     torch.cuda.synchronize()
@@ -125,6 +125,12 @@ def run(case, layers, reps, fsdp=8):
         b.synchronize()
         times.append(a.elapsed_time(b))
     ms = statistics.median(times)
+    torch.cuda.synchronize(0)
+    if case == "nvlink_fanout":  # the peer stores really landed
+        chunk, target = keep[0], keep[1]
+        crow = chunk.shape[0]
+        for k in range(4):
+            assert torch.equal(target[k * crow:(k + 1) * crow].cpu(), chunk.cpu()), "fan-out mismatch"
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     achieved = 2 * moved / (ms / 1e3) / 1e9
