@@ -621,6 +621,31 @@ def run_c5(args) -> dict:
     return result
 
 
+def time_launch(fn, gpu: int, reps: int = 5, warmup: int = 3) -> tuple[float, float]:
+    """(median kernel ms by CUDA events on the launching stream, median host enqueue ms).
+    The stream is held by a short device-side sleep while the host enqueues, so the event
+    window contains the kernel only."""
+    import torch
+
+    with torch.cuda.device(gpu):
+        stream = torch.cuda.current_stream(gpu)
+        for _ in range(warmup):
+            fn(stream)
+        torch.cuda.synchronize(gpu)
+        dev_ms, host_ms = [], []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(20_000_000)  # ~10 ms of GPU time covers the host enqueue
+            a.record(stream)
+            t0 = time.perf_counter()
+            fn(stream)
+            host_ms.append((time.perf_counter() - t0) * 1e3)
+            b.record(stream)
+            b.synchronize()
+            dev_ms.append(a.elapsed_time(b))
+    return statistics.median(dev_ms), statistics.median(host_ms)
+
+
 def kernel_roofline(tv, native, state, rt, d) -> dict:
     """The box-copy kernel as the device snapshot of an async save: every local shard
     packed into one arena, ONE launch per GPU; algorithmic bytes = 2 × bytes copied."""
@@ -646,19 +671,7 @@ def kernel_roofline(tv, native, state, rt, d) -> dict:
         [(0,) * t.dim() for t in regions], [tuple(t.shape) for t in regions],
         [t.element_size() for t in regions],
     )
-    stream = torch.cuda.current_stream(gpu)
-    for _ in range(3):
-        native.copy_boxes(gpu, copies, stream.cuda_stream)
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(5):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        native.copy_boxes(gpu, copies, stream.cuda_stream)
-        b.record(stream)
-        b.synchronize()
-        times.append(a.elapsed_time(b))
-    ms = statistics.median(times)
+    ms, host_ms = time_launch(lambda s: native.copy_boxes(gpu, copies, s.cuda_stream), gpu)
     achieved = 2 * total / (ms / 1e3) / 1e9
     peak = measured_peaks()["hbm_gbs"]
     del arena
@@ -672,6 +685,7 @@ def kernel_roofline(tv, native, state, rt, d) -> dict:
         "traffic": None,
         "bytes_per_launch": 2 * total,
         "ms_per_launch": round(ms, 3),
+        "host_enqueue_ms": round(host_ms, 3),
         "launches_in_timed_region": 0,
     }
 
@@ -759,7 +773,8 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
 
     import treevault_oracle as orc
 
-    P = processes or 8
+    cores = len(os.sched_getaffinity(0))
+    P = processes or max(1, min(64, 1 << (cores.bit_length() - 1)))  # all host threads (power of 2)
     dims = dict(LLAMA3_8B)
     dims["layers"] = sample_layers
     leaves = [(t, p, s, dt) for t, p, s, dt in llama_leaves(**dims)
@@ -813,7 +828,7 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
 
 def run_reference(args) -> dict:
     d = Dist()
-    res = cpu_baseline(args, sample_layers=args.cpu_layers, processes=8,
+    res = cpu_baseline(args, sample_layers=args.cpu_layers,
                        root_dir=prepare_storage(args, d) if args.storage != "shm" else None)
     return {
         "impl": "reference",

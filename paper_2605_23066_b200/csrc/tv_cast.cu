@@ -11,8 +11,10 @@
 // bool never converts (rejected by the planner, like the reference).
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "tv_internal.h"
 
@@ -22,14 +24,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kPerLane = 8;
-constexpr int kSeg = 32 * kPerLane;     // elements per warp unit (mode 0)
 constexpr int kFlatPer = 4;
 constexpr int kFlat = kThreads * kFlatPer;
-
-__device__ __forceinline__ bool is_float(int dt) {
-  return dt == TV_DT_F32 || dt == TV_DT_F64 || dt == TV_DT_BF16;
-}
 
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) {
   return __uint_as_float(((uint32_t)b) << 16);
@@ -41,83 +37,6 @@ __device__ __forceinline__ uint16_t f32_to_bf16(float f) {
     return (uint16_t)((bits >> 16) | 0x40);
   uint64_t r = ((uint64_t)bits + 0x7fffu + ((bits >> 16) & 1u)) >> 16;
   return (uint16_t)r;
-}
-
-struct Value {
-  double f;    // float sources
-  long long i; // integer sources
-};
-
-__device__ __forceinline__ Value load_value(const char* p, int dt) {
-  Value v{0.0, 0};
-  switch (dt) {
-    case TV_DT_F32: v.f = (double)*reinterpret_cast<const float*>(p); break;
-    case TV_DT_F64: v.f = *reinterpret_cast<const double*>(p); break;
-    case TV_DT_BF16: v.f = (double)bf16_to_f32(*reinterpret_cast<const uint16_t*>(p)); break;
-    case TV_DT_I32: v.i = *reinterpret_cast<const int32_t*>(p); break;
-    case TV_DT_I64: v.i = *reinterpret_cast<const long long*>(p); break;
-    case TV_DT_U8: v.i = *reinterpret_cast<const uint8_t*>(p); break;
-    default: v.i = *reinterpret_cast<const uint8_t*>(p); break;
-  }
-  return v;
-}
-
-__device__ __forceinline__ void int_range(int dt, long long& lo, long long& hi) {
-  switch (dt) {
-    case TV_DT_I32: lo = INT32_MIN; hi = INT32_MAX; break;
-    case TV_DT_U8: lo = 0; hi = 255; break;
-    default: lo = LLONG_MIN; hi = LLONG_MAX; break;
-  }
-}
-
-// Convert one element; returns TV_CAST_* bits of a violated check.
-__device__ __forceinline__ uint32_t convert(const char* sp, char* dp, int sdt, int ddt) {
-  const Value v = load_value(sp, sdt);
-  uint32_t bad = 0;
-  if (is_float(sdt)) {
-    const double x = v.f;
-    switch (ddt) {
-      case TV_DT_F32: *reinterpret_cast<float*>(dp) = __double2float_rn(x); break;
-      case TV_DT_F64: *reinterpret_cast<double*>(dp) = x; break;
-      case TV_DT_BF16:
-        *reinterpret_cast<uint16_t*>(dp) = f32_to_bf16(sdt == TV_DT_F64 ? __double2float_rn(x) : (float)x);
-        break;
-      default: {  // float -> int, checked
-        long long lo, hi;
-        int_range(ddt, lo, hi);
-        long long q = 0;
-        if (!isfinite(x)) {
-          bad |= TV_CAST_NONFINITE;
-        } else if (x != floor(x)) {
-          bad |= TV_CAST_NONINTEGRAL;
-        } else if (ddt == TV_DT_I64 ? (x >= 9223372036854775808.0 || x < -9223372036854775808.0)
-                                    : (x < (double)lo || x > (double)hi)) {
-          bad |= TV_CAST_OVERFLOW;
-        } else {
-          q = (long long)x;
-        }
-        if (ddt == TV_DT_I32) *reinterpret_cast<int32_t*>(dp) = (int32_t)q;
-        else if (ddt == TV_DT_I64) *reinterpret_cast<long long*>(dp) = q;
-        else *reinterpret_cast<uint8_t*>(dp) = (uint8_t)q;
-      }
-    }
-  } else {
-    const long long x = v.i;
-    switch (ddt) {
-      case TV_DT_F32: *reinterpret_cast<float*>(dp) = __ll2float_rn(x); break;
-      case TV_DT_F64: *reinterpret_cast<double*>(dp) = __ll2double_rn(x); break;
-      case TV_DT_BF16: *reinterpret_cast<uint16_t*>(dp) = f32_to_bf16(__ll2float_rn(x)); break;
-      default: {  // int -> int, checked
-        long long lo, hi;
-        int_range(ddt, lo, hi);
-        if (x < lo || x > hi) bad |= TV_CAST_OVERFLOW;
-        if (ddt == TV_DT_I32) *reinterpret_cast<int32_t*>(dp) = (int32_t)x;
-        else if (ddt == TV_DT_I64) *reinterpret_cast<long long*>(dp) = x;
-        else *reinterpret_cast<uint8_t*>(dp) = (uint8_t)x;
-      }
-    }
-  }
-  return bad;
 }
 
 __device__ __forceinline__ int find_cast_job(const CastJob* jobs, int n, int64_t block) {
@@ -137,47 +56,176 @@ __device__ __forceinline__ void origin(const CastJob& j, int64_t r, int64_t& so,
   dof = i0 * j.ds[0] + i1 * j.ds[1] + i2 * j.ds[2];
 }
 
+// ---- typed conversion (the hot loop is specialised per dtype pair) ------------------------
+
+struct BF16 {
+  uint16_t bits;
+};
+
+template <typename T> struct Kind;  // 0 = float, 1 = integer
+template <> struct Kind<float> { static constexpr int v = 0; };
+template <> struct Kind<double> { static constexpr int v = 0; };
+template <> struct Kind<BF16> { static constexpr int v = 0; };
+template <> struct Kind<int32_t> { static constexpr int v = 1; };
+template <> struct Kind<long long> { static constexpr int v = 1; };
+template <> struct Kind<uint8_t> { static constexpr int v = 1; };
+
+__device__ __forceinline__ double as_double(float x) { return (double)x; }
+__device__ __forceinline__ double as_double(double x) { return x; }
+__device__ __forceinline__ double as_double(BF16 x) { return (double)bf16_to_f32(x.bits); }
+__device__ __forceinline__ long long as_ll(int32_t x) { return x; }
+__device__ __forceinline__ long long as_ll(long long x) { return x; }
+__device__ __forceinline__ long long as_ll(uint8_t x) { return x; }
+
+template <typename D> struct Narrow;
+template <> struct Narrow<int32_t> {
+  static constexpr long long lo = INT32_MIN, hi = INT32_MAX;
+};
+template <> struct Narrow<long long> {
+  static constexpr long long lo = LLONG_MIN, hi = LLONG_MAX;
+};
+template <> struct Narrow<uint8_t> {
+  static constexpr long long lo = 0, hi = 255;
+};
+
+// float source -> float destination
+__device__ __forceinline__ float f2f(double x, float*) { return __double2float_rn(x); }
+__device__ __forceinline__ double f2f(double x, double*) { return x; }
+
+template <typename S, typename D>
+__device__ __forceinline__ D cvt(S x, uint32_t& bad) {
+  if constexpr (Kind<S>::v == 0 && Kind<D>::v == 0) {
+    if constexpr (std::is_same<D, BF16>::value) {
+      float f;
+      if constexpr (std::is_same<S, double>::value) f = __double2float_rn(x);
+      else if constexpr (std::is_same<S, float>::value) f = x;
+      else f = bf16_to_f32(x.bits);
+      return BF16{f32_to_bf16(f)};
+    } else if constexpr (std::is_same<S, float>::value && std::is_same<D, float>::value) {
+      return x;
+    } else {
+      return f2f(as_double(x), (D*)nullptr);
+    }
+  } else if constexpr (Kind<S>::v == 0) {  // float -> int (checked)
+    const double v = as_double(x);
+    if (!isfinite(v)) {
+      bad |= TV_CAST_NONFINITE;
+      return D(0);
+    }
+    if (v != floor(v)) {
+      bad |= TV_CAST_NONINTEGRAL;
+      return D(0);
+    }
+    const bool over = std::is_same<D, long long>::value
+                          ? (v >= 9223372036854775808.0 || v < -9223372036854775808.0)
+                          : (v < (double)Narrow<D>::lo || v > (double)Narrow<D>::hi);
+    if (over) {
+      bad |= TV_CAST_OVERFLOW;
+      return D(0);
+    }
+    return (D)(long long)v;
+  } else if constexpr (Kind<D>::v == 0) {  // int -> float
+    const long long v = as_ll(x);
+    if constexpr (std::is_same<D, BF16>::value) return BF16{f32_to_bf16(__ll2float_rn(v))};
+    else if constexpr (std::is_same<D, float>::value) return __ll2float_rn(v);
+    else return __ll2double_rn(v);
+  } else {  // int -> int (checked)
+    const long long v = as_ll(x);
+    if (v < Narrow<D>::lo || v > Narrow<D>::hi) bad |= TV_CAST_OVERFLOW;
+    return (D)v;
+  }
+}
+
+template <typename T, int N>
+struct alignas(sizeof(T) * N) Pack {
+  T v[N];
+};
+
+// Mode 0: a warp converts one segment of a run, 4 consecutive elements per lane-step,
+// moved as one vector load / store when both addresses are aligned for it.
+constexpr int kVec = 4;
+constexpr int kSegV = 32 * kVec * 4;  // elements per warp unit
+
+template <typename S, typename D>
+__device__ __forceinline__ void cast_segment(const CastJob& j, int64_t local, uint32_t& bad) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t segs = (j.run + kSegV - 1) / kSegV;
+  const int64_t unit = local * kWarps + warp;
+  if (unit >= j.nruns * segs) return;
+  const int64_t r = unit / segs, sg = unit - r * segs;
+  int64_t so, dof;
+  origin(j, r, so, dof);
+  const S* src = reinterpret_cast<const S*>(j.src + so) + sg * kSegV;
+  D* dst = reinterpret_cast<D*>(j.dst + dof) + sg * kSegV;
+  const int64_t left = j.run - sg * kSegV;
+  const int nv = (int)(left < kSegV ? left : kSegV);
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) % sizeof(Pack<S, kVec>)) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dst) % sizeof(Pack<D, kVec>)) == 0);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = (lane + 32 * u) * kVec;
+    if (e >= nv) break;
+    if (vec && e + kVec <= nv) {
+      const Pack<S, kVec> in = *reinterpret_cast<const Pack<S, kVec>*>(src + e);
+      Pack<D, kVec> out;
+#pragma unroll
+      for (int k = 0; k < kVec; ++k) out.v[k] = cvt<S, D>(in.v[k], bad);
+      *reinterpret_cast<Pack<D, kVec>*>(dst + e) = out;
+    } else {
+      for (int k = 0; k < kVec && e + k < nv; ++k) dst[e + k] = cvt<S, D>(src[e + k], bad);
+    }
+  }
+}
+
+template <typename S, typename D>
+__device__ __forceinline__ void cast_flat(const CastJob& j, int64_t local, uint32_t& bad) {
+  const int64_t total = j.nruns * j.run;
+#pragma unroll
+  for (int k = 0; k < kFlatPer; ++k) {
+    const int64_t v = local * kFlat + k * kThreads + threadIdx.x;
+    if (v < total) {
+      const int64_t r = v / j.run, w = v - r * j.run;
+      int64_t so, dof;
+      origin(j, r, so, dof);
+      reinterpret_cast<D*>(j.dst + dof)[w] = cvt<S, D>(reinterpret_cast<const S*>(j.src + so)[w], bad);
+    }
+  }
+}
+
+template <typename S, typename D>
+__device__ __forceinline__ void cast_job(const CastJob& j, int64_t local, uint32_t& bad) {
+  if (j.mode == 0) cast_segment<S, D>(j, local, bad);
+  else cast_flat<S, D>(j, local, bad);
+}
+
+template <typename S>
+__device__ __forceinline__ void cast_dst(const CastJob& j, int64_t local, uint32_t& bad) {
+  switch (j.ddt) {
+    case TV_DT_F32: cast_job<S, float>(j, local, bad); break;
+    case TV_DT_F64: cast_job<S, double>(j, local, bad); break;
+    case TV_DT_BF16: cast_job<S, BF16>(j, local, bad); break;
+    case TV_DT_I32: cast_job<S, int32_t>(j, local, bad); break;
+    case TV_DT_I64: cast_job<S, long long>(j, local, bad); break;
+    case TV_DT_U8: cast_job<S, uint8_t>(j, local, bad); break;
+    default: break;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) box_cast_kernel(const CastJob* __restrict__ jobs,
                                                             int n_jobs, int64_t block0) {
   const int64_t block = block0 + blockIdx.x;
   const CastJob j = jobs[find_cast_job(jobs, n_jobs, block)];
   const int64_t local = block - j.unit_begin;
-  const int ssz = j.sdt == TV_DT_F64 || j.sdt == TV_DT_I64 ? 8 : j.sdt == TV_DT_F32 || j.sdt == TV_DT_I32 ? 4
-                  : j.sdt == TV_DT_BF16 ? 2 : 1;
-  const int dsz = j.ddt == TV_DT_F64 || j.ddt == TV_DT_I64 ? 8 : j.ddt == TV_DT_F32 || j.ddt == TV_DT_I32 ? 4
-                  : j.ddt == TV_DT_BF16 ? 2 : 1;
   uint32_t bad = 0;
   if (local < j.units) {
-    if (j.mode == 0) {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      const int64_t segs = (j.run + kSeg - 1) / kSeg;
-      const int64_t unit = local * kWarps + warp;
-      if (unit < j.nruns * segs) {
-        const int64_t r = unit / segs, s = unit - r * segs;
-        int64_t so, dof;
-        origin(j, r, so, dof);
-        const int64_t e0 = s * kSeg;
-        const int64_t left = j.run - e0;
-        const int nv = (int)(left < kSeg ? left : kSeg);
-#pragma unroll
-        for (int k = 0; k < kPerLane; ++k) {
-          const int idx = lane + 32 * k;
-          if (idx < nv)
-            bad |= convert(j.src + so + (e0 + idx) * ssz, j.dst + dof + (e0 + idx) * dsz, j.sdt, j.ddt);
-        }
-      }
-    } else {
-      const int64_t total = j.nruns * j.run;
-#pragma unroll
-      for (int k = 0; k < kFlatPer; ++k) {
-        const int64_t v = local * kFlat + k * kThreads + threadIdx.x;
-        if (v < total) {
-          const int64_t r = v / j.run, w = v - r * j.run;
-          int64_t so, dof;
-          origin(j, r, so, dof);
-          bad |= convert(j.src + so + w * ssz, j.dst + dof + w * dsz, j.sdt, j.ddt);
-        }
-      }
+    switch (j.sdt) {
+      case TV_DT_F32: cast_dst<float>(j, local, bad); break;
+      case TV_DT_F64: cast_dst<double>(j, local, bad); break;
+      case TV_DT_BF16: cast_dst<BF16>(j, local, bad); break;
+      case TV_DT_I32: cast_dst<int32_t>(j, local, bad); break;
+      case TV_DT_I64: cast_dst<long long>(j, local, bad); break;
+      case TV_DT_U8: cast_dst<uint8_t>(j, local, bad); break;
+      default: break;
     }
   }
   bad = __reduce_or_sync(0xffffffffu, bad);
@@ -280,7 +328,7 @@ int64_t plan_cast_units(std::vector<CastJob>& jobs) {
   int64_t total = 0;
   for (auto& j : jobs) {
     if (j.mode == 0) {
-      const int64_t segs = (j.run + kSeg - 1) / kSeg;
+      const int64_t segs = (j.run + kSegV - 1) / kSegV;
       j.units = (j.nruns * segs + kWarps - 1) / kWarps;
     } else {
       j.units = (j.nruns * j.run + kFlat - 1) / kFlat;

@@ -112,19 +112,9 @@ def run(case, layers, reps, fsdp=8):
         copies, moved, keep = make_fanout(layers)
     else:
         copies, moved, keep = make_case(case, layers, fsdp)
-    stream = torch.cuda.current_stream(0)
-    for _ in range(3):
-        native.copy_boxes(0, copies, stream.cuda_stream)
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        native.copy_boxes(0, copies, stream.cuda_stream)
-        b.record(stream)
-        b.synchronize()
-        times.append(a.elapsed_time(b))
-    ms = statistics.median(times)
+    from bench import time_launch
+
+    ms, host_ms = time_launch(lambda st: native.copy_boxes(0, copies, st.cuda_stream), 0, reps=reps)
     torch.cuda.synchronize(0)
     if case == "nvlink_fanout":  # the peer stores really landed
         chunk, target = keep[0], keep[1]
@@ -142,6 +132,7 @@ def run(case, layers, reps, fsdp=8):
                 "nvlink_GBps": round(nv, 1), "peak_GBps": 770.0, "frac": round(nv / 770.0, 4),
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
     return {"case": case, "copies": len(copies), "bytes_moved": moved, "ms": round(ms, 3),
+            "host_enqueue_ms": round(host_ms, 3),
             "achieved_GBps": round(achieved, 1), "peak_GBps": peak, "frac": round(achieved / peak, 4)}
 
 
