@@ -141,10 +141,13 @@ struct alignas(sizeof(T) * N) Pack {
   T v[N];
 };
 
-// Mode 0: a warp converts one segment of a run, 4 consecutive elements per lane-step,
-// moved as one vector load / store when both addresses are aligned for it.
+// Mode 0: a warp converts one segment of a run.  Full, aligned segments take the fast
+// path: every lane first issues kU 4-element vector loads (ILP: kU*16 B in flight per lane
+// for f32), then converts and stores them; tails / misaligned runs go element by element
+// (still coalesced across the warp).
 constexpr int kVec = 4;
-constexpr int kSegV = 32 * kVec * 4;  // elements per warp unit
+constexpr int kU = 8;
+constexpr int kSegV = 32 * kVec * kU;  // elements per warp unit
 
 template <typename S, typename D>
 __device__ __forceinline__ void cast_segment(const CastJob& j, int64_t local, uint32_t& bad) {
@@ -159,22 +162,24 @@ __device__ __forceinline__ void cast_segment(const CastJob& j, int64_t local, ui
   D* dst = reinterpret_cast<D*>(j.dst + dof) + sg * kSegV;
   const int64_t left = j.run - sg * kSegV;
   const int nv = (int)(left < kSegV ? left : kSegV);
-  const bool vec = ((reinterpret_cast<uintptr_t>(src) % sizeof(Pack<S, kVec>)) == 0) &&
+  const bool vec = nv == kSegV &&
+                   ((reinterpret_cast<uintptr_t>(src) % sizeof(Pack<S, kVec>)) == 0) &&
                    ((reinterpret_cast<uintptr_t>(dst) % sizeof(Pack<D, kVec>)) == 0);
+  if (vec) {
+    Pack<S, kVec> in[kU];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int e = (lane + 32 * u) * kVec;
-    if (e >= nv) break;
-    if (vec && e + kVec <= nv) {
-      const Pack<S, kVec> in = *reinterpret_cast<const Pack<S, kVec>*>(src + e);
+    for (int u = 0; u < kU; ++u)
+      in[u] = *reinterpret_cast<const Pack<S, kVec>*>(src + (lane + 32 * u) * kVec);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
       Pack<D, kVec> out;
 #pragma unroll
-      for (int k = 0; k < kVec; ++k) out.v[k] = cvt<S, D>(in.v[k], bad);
-      *reinterpret_cast<Pack<D, kVec>*>(dst + e) = out;
-    } else {
-      for (int k = 0; k < kVec && e + k < nv; ++k) dst[e + k] = cvt<S, D>(src[e + k], bad);
+      for (int k = 0; k < kVec; ++k) out.v[k] = cvt<S, D>(in[u].v[k], bad);
+      *reinterpret_cast<Pack<D, kVec>*>(dst + (lane + 32 * u) * kVec) = out;
     }
+    return;
   }
+  for (int e = lane; e < nv; e += 32) dst[e] = cvt<S, D>(src[e], bad);
 }
 
 template <typename S, typename D>

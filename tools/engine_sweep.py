@@ -41,9 +41,11 @@ def main():
                 (4 << 20, 32, cores), (4 << 20, 64, cores), (1 << 20, 128, cores)]
     if args.quick:
         settings += [(4 << 20, 16, cores), (16 << 20, 16, cores), (8 << 20, 32, cores // 2)]
-    if args.settings:
-        settings = [(int(float(a) * (1 << 20)), int(b), cores)
-                    for a, b in (x.split(":") for x in args.settings.split(","))]
+    if args.settings:  # slotMiB:count[:threads]
+        settings = []
+        for x in args.settings.split(","):
+            f = x.split(":")
+            settings.append((int(float(f[0]) * (1 << 20)), int(f[1]), int(f[2]) if len(f) > 2 else cores))
     i = 0
     results = {}
     # interleave settings across repetitions so slow drift of the box hits all of them
