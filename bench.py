@@ -434,6 +434,9 @@ def run_ours(args) -> dict:
             "thread_wait_dma_s": round(a["seconds_wait_dma"] - b["seconds_wait_dma"], 3),
             "producer_wait_slot_s": round(a["seconds_wait_slot"] - b["seconds_wait_slot"], 3),
             "storage_GB": round((a["bytes_storage"] - b["bytes_storage"]) / 1e9, 3),
+            "pcie_GB": round((a["bytes_device"] - b["bytes_device"]) / 1e9, 3),
+            # save: bytes packed by the kernel; load: bytes the unpack / NVLink fan-out moved
+            "kernel_GB": round((a["bytes_packed"] - b["bytes_packed"]) / 1e9, 3),
         }
     save_ms = statistics.mean(saves)
     restore_ms = statistics.mean(restores)

@@ -145,12 +145,15 @@ struct alignas(sizeof(T) * N) Pack {
 // path: every lane first issues kU 4-element vector loads (ILP: kU*16 B in flight per lane
 // for f32), then converts and stores them; tails / misaligned runs go element by element
 // (still coalesced across the warp).
-constexpr int kVec = 4;
-constexpr int kU = 8;
-constexpr int kSegV = 32 * kVec * kU;  // elements per warp unit
+constexpr int kSegV = 1024;  // elements per warp unit
 
 template <typename S, typename D>
 __device__ __forceinline__ void cast_segment(const CastJob& j, int64_t local, uint32_t& bad) {
+  // Vector width: the narrower side moves 16 bytes per access (f32->bf16: 8 elements =
+  // 32 B loaded, 16 B stored per lane-step).
+  constexpr int kVec = 16 / (sizeof(S) < sizeof(D) ? sizeof(S) : sizeof(D)) > 8
+                           ? 8 : 16 / (sizeof(S) < sizeof(D) ? sizeof(S) : sizeof(D));
+  constexpr int kU = kSegV / (32 * kVec);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t segs = (j.run + kSegV - 1) / kSegV;
   const int64_t unit = local * kWarps + warp;

@@ -359,7 +359,8 @@ class EngineConfig:
     """Pipeline sizing.
 
     threads  — host cores shared by the engines running at once on this box (the
-               threads runtime's processes, or torchrun's LOCAL_WORLD_SIZE ranks);
+               threads runtime's processes, or torchrun's LOCAL_WORLD_SIZE ranks), minus
+               one core per engine for its producer;
     n_slots  — 2 pinned slots per storage thread (fewer starves the readers);
     slot     — 2 MiB, or 1 MiB when the rings of all engines would not fit the host's
                last-level cache: the DMA'd bytes are re-read by pwrite / the H2D straight
@@ -379,9 +380,12 @@ class EngineConfig:
         return max(concurrent, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
 
     def threads_for(self, concurrent: int) -> int:
+        """Storage threads per engine: the host's cores minus one per engine (its producer
+        thread and the CUDA driver need a core; measured better than all cores)."""
         if self.threads:
             return self.threads
-        return max(2, _host_cores() // self._engines(concurrent))
+        engines = self._engines(concurrent)
+        return max(2, (_host_cores() - engines) // engines)
 
     def sizing(self, concurrent: int) -> tuple[int, int, int, int]:
         """(n_slots, slot_bytes, staging_bytes, threads) for an engine of this box."""
