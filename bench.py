@@ -6,7 +6,9 @@
 Default workload (BASELINE.json configs[1], "C2"): Llama-3-8B-shaped state — bf16
 params + fp32 Adam mu/nu, 873 leaves, 80,302,612,480 bytes — FSDP-sharded on dim 0 over
 the N GPUs (one logical process per GPU), synthetic random values generated on device.
-One step = a synchronous ``save_checkpoint`` (call → committed on /dev/shm) followed by a
+One step = an asynchronous ``save_checkpoint`` (Orbax's training default: the blocking
+device snapshot, then ``wait()`` for pack/D2H/write/commit on /dev/shm; ``--save-mode
+sync`` for the zero-copy synchronous save) followed by a
 ``load_checkpoint`` of the same checkpoint (call → every shard resident in HBM).
 
 value = 2 × tree bytes / step time (GB/s; each byte is saved once and restored once),
@@ -275,12 +277,12 @@ def make_workload(tv, args, N) -> Workload:
         leaves = [("model", f"a{i}", (4096, 4096), "f32") for i in range(4)]
         mesh = tv.Mesh.create([("solo", 1)], process_count=1)
         return Workload(tv, "c1", leaves, mesh, lambda s: None, tv.SaveOptions(sync=True),
-                        describe="C1 4 x (4096,4096) f32 unsharded, process 0 writes, sync save -> restore")
+                        describe="C1 4 x (4096,4096) f32 unsharded, process 0 writes, " + args.save_mode + " save -> restore")
     if cfg == "c2":
         mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
         return Workload(tv, "c2", llama, mesh, fsdp_spec, tv.SaveOptions(sync=True),
                         describe=f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu, FSDP-{N} on dim 0, "
-                                 "sync save -> restore, per_leaf layout")
+                                 f"{args.save_mode} save -> restore, per_leaf layout")
     if cfg in ("c3", "c3ss"):
         if N % 2:
             raise SystemExit("c3 needs an even number of GPUs (replica 2 x fsdp N/2)")
@@ -288,7 +290,7 @@ def make_workload(tv, args, N) -> Workload:
         rp = cfg == "c3"
         return Workload(tv, cfg, llama, mesh, fsdp_spec, tv.SaveOptions(sync=True, replica_parallel=rp),
                         describe=f"C3 Llama-3-8B on a 2x{N // 2} (replica x fsdp) mesh, "
-                                 f"{'replica-parallel' if rp else 'single-slice'} sync save -> restore")
+                                 f"{'replica-parallel' if rp else 'single-slice'} {args.save_mode} save -> restore")
     if cfg == "c4":
         if N % 2:
             raise SystemExit("c4 needs an even number of GPUs")
@@ -364,7 +366,18 @@ def run_ours(args) -> dict:
     torch.cuda.synchronize()
     tree_bytes = wl.tree_bytes
 
-    def step(i: int):
+    import dataclasses
+
+    sync_opts = dataclasses.replace(wl.save_options, sync=True)
+    async_opts = dataclasses.replace(wl.save_options, sync=False)
+    step_opts = async_opts if args.save_mode == "async" else sync_opts
+
+    def step(i: int, opts=None):
+        """One save (call -> committed) + one restore (call -> every shard resident).
+        Async mode (Orbax's default for training): the blocking device snapshot, then
+        wait() for the background pack/D2H/write/commit.  Returns (save ms, restore ms,
+        save wall ms, restore wall ms, blocking ms)."""
+        opts = opts or step_opts
         path = f"bench/step_{i:04d}"
         d.barrier()
         torch.cuda.synchronize()
@@ -373,7 +386,9 @@ def run_ours(args) -> dict:
         ev2 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         ev0.record()
-        tv.save_checkpoint(rt, path, state, shardings, wl.save_options).wait()
+        handle = tv.save_checkpoint(rt, path, state, shardings, opts)
+        tb = time.perf_counter()
+        handle.wait()
         ev1.record()
         t1 = time.perf_counter()
         if abstract is None:
@@ -388,7 +403,8 @@ def run_ours(args) -> dict:
         if d.rank == 0:
             shutil.rmtree(os.path.join(base, path), ignore_errors=True)
         d.barrier()
-        return ev0.elapsed_time(ev1), ev1.elapsed_time(ev2), (t1 - t0) * 1e3, (t2 - t1) * 1e3
+        return (ev0.elapsed_time(ev1), ev1.elapsed_time(ev2), (t1 - t0) * 1e3, (t2 - t1) * 1e3,
+                (tb - t0) * 1e3)
 
     for i in range(args.warmup):
         step(i)
@@ -414,12 +430,16 @@ def run_ours(args) -> dict:
     if d.rank == 0:
         clocks.start()
     before = native.totals()
-    saves, restores, walls = [], [], []
+    native.kernel_timing(True)
+    saves, restores, walls, blocks = [], [], [], []
     for i in range(args.steps):
-        s_ms, r_ms, ws, wr = step(args.warmup + i)
+        s_ms, r_ms, ws, wr, b_ms = step(args.warmup + i)
         saves.append(d.max(s_ms))
         restores.append(d.max(r_ms))
         walls.append(d.max(ws + wr))
+        blocks.append(d.max(b_ms))
+    native.kernel_timing(False)
+    ktime = native.kernel_timing_collect()
     after = native.totals()
     clock_info = clocks.stop() if d.rank == 0 else {}
     kernels = d.sum(after["kernel_launches"] - before["kernel_launches"])
@@ -445,20 +465,23 @@ def run_ours(args) -> dict:
     save_gbs = tree_bytes / (save_ms / 1e3) / 1e9
     restore_gbs = tree_bytes / (restore_ms / 1e3) / 1e9
 
-    # async-save blocking vs the sync save it replaces
-    d.barrier()
-    torch.cuda.synchronize()
-    async_opts = tv.SaveOptions(sync=False, replica_parallel=wl.save_options.replica_parallel)
-    t0 = time.perf_counter()
-    handle = tv.save_checkpoint(rt, "bench/async", state, shardings, async_opts)
-    blocking_ms = d.max((time.perf_counter() - t0) * 1e3)
-    handle.wait()
-    async_total_ms = d.max((time.perf_counter() - t0) * 1e3)
+    # async-save blocking vs the synchronous save it replaces: the timed steps give one
+    # side, one extra save (untimed for `value`) in the other mode gives the other
+    if args.save_mode == "async":
+        blocking_ms = statistics.mean(blocks)
+        other = step(args.warmup + args.steps, sync_opts)
+        sync_save_ms = d.max(other[0])
+        async_total_ms = save_ms
+    else:
+        sync_save_ms = save_ms
+        other = step(args.warmup + args.steps, async_opts)
+        blocking_ms = d.max(other[4])
+        async_total_ms = d.max(other[0])
     d.barrier()
     if d.rank == 0:
         shutil.rmtree(os.path.join(base, "bench"), ignore_errors=True)
 
-    kern = kernel_roofline(tv, native, state, rt, d)
+    kern = kernel_roofline(tv, native, state, rt, d, ktime, args, step_ms)
     e2e = end_to_end(tv, rt, wl, args, d, base) if not args.no_e2e else None
 
     peaks = measured_peaks()
@@ -490,9 +513,11 @@ def run_ours(args) -> dict:
         "save_ms": round(save_ms, 2),
         "restore_ms": round(restore_ms, 2),
         "wall_ms_per_step": round(statistics.mean(walls), 2),
+        "save_mode": args.save_mode,
         "async_blocking_ms": round(blocking_ms, 2),
         "async_total_ms": round(async_total_ms, 2),
-        "async_blocking_frac_of_sync_save": round(blocking_ms / save_ms, 4),
+        "sync_save_ms": round(sync_save_ms, 2),
+        "async_blocking_frac_of_sync_save": round(blocking_ms / sync_save_ms, 4),
         "io_roofline": None,
         "roofline": kern,
         "e2e": e2e,
@@ -502,7 +527,7 @@ def run_ours(args) -> dict:
             "copy_engine_dma_by_libtvgpu": int(dmas),
             "note": "contiguous chunk payloads move by copy-engine DMA issued by libtvgpu's engine "
                     "(measured faster than SM-driven PCIe: profiles/r01_pcie_kernel_vs_ce.jsonl); "
-                    "strided boxes, snapshots and reshard scatters run box_copy_kernel",
+                    "async-save snapshots, strided boxes and reshard scatters run box_copy_kernel",
         },
         "clocks": clock_info,
         "engine_rank0": engine,
@@ -649,10 +674,57 @@ def time_launch(fn, gpu: int, reps: int = 5, warmup: int = 3) -> tuple[float, fl
     return statistics.median(dev_ms), statistics.median(host_ms)
 
 
-def kernel_roofline(tv, native, state, rt, d) -> dict:
-    """The box-copy kernel as the device snapshot of an async save: every local shard
-    packed into one arena, ONE launch per GPU; algorithmic bytes = 2 × bytes copied."""
+def _ncu_traffic(bytes_per_launch: int):
+    """DRAM bytes per launch of the same kernel launch from a committed ncu capture
+    (profiles/r01_roofline_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum),
+    used only when that capture's launch moved exactly the bytes this one did."""
+    path = os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as f:
+        rows = json.load(f).get("launches", [])
+    for r in rows:
+        if int(r["algorithmic_bytes"]) == int(bytes_per_launch):
+            return int(r["dram_read_bytes"]) + int(r["dram_write_bytes"]), r.get("source")
+    return None, None
+
+
+def kernel_roofline(tv, native, state, rt, d, ktime: dict, args, step_ms: float) -> dict:
+    """The box-copy kernel inside the timed steps (async mode: the device snapshot of each
+    save, ONE launch per GPU per step), timed live by libtvgpu with CUDA events on the
+    launching stream (tv_kernel_timing); algorithmic bytes = 2 × bytes copied.  In sync
+    mode no kernel runs in the timed region (contiguous payloads go by DMA), so the same
+    snapshot launch is timed standalone and marked launches_in_timed_region = 0."""
     import torch
+
+    peak = measured_peaks()["hbm_gbs"]
+    launches = int(d.sum(ktime["launches"]))
+    if launches > 0:
+        ms_total = d.sum(ktime["ms_total"])
+        nbytes = d.sum(ktime["bytes"])
+        per_launch = int(round(nbytes / launches))
+        ms = ms_total / launches
+        achieved = nbytes / (ms_total / 1e3) / 1e9
+        traffic, src = _ncu_traffic(per_launch)
+        world = d.world if d.on else 1
+        return {
+            "kernel": "box_copy_kernel (async-save device snapshot: this GPU's write ranges -> arena, "
+                      "1 launch per GPU per step)",
+            "bound": "hbm",
+            "achieved": round(achieved, 1),
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "traffic_source": src,
+            "bytes_per_launch": per_launch,
+            "ms_per_launch": round(ms, 3),
+            "ms_max_launch": round(d.max(ktime["ms_max"]), 3),
+            "launches_in_timed_region": launches,
+            "share_of_step": round(ms_total / world / args.steps / step_ms, 5),
+            "timing": "CUDA events on the launching stream around every launch in the timed steps "
+                      "(libtvgpu tv_kernel_timing), summed over ranks",
+        }
 
     regions = []
     for tree in state.values():
@@ -676,16 +748,17 @@ def kernel_roofline(tv, native, state, rt, d) -> dict:
     )
     ms, host_ms = time_launch(lambda s: native.copy_boxes(gpu, copies, s.cuda_stream), gpu)
     achieved = 2 * total / (ms / 1e3) / 1e9
-    peak = measured_peaks()["hbm_gbs"]
     del arena
+    traffic, src = _ncu_traffic(2 * total)
     return {
-        "kernel": "box_copy_kernel (device snapshot: all local shards -> arena, 1 launch)",
+        "kernel": "box_copy_kernel (device snapshot: all local shards -> arena, 1 launch, standalone)",
         "bound": "hbm",
         "achieved": round(achieved, 1),
         "peak": peak,
         "unit": "GB/s",
         "frac": round(achieved / peak, 4),
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_source": src,
         "bytes_per_launch": 2 * total,
         "ms_per_launch": round(ms, 3),
         "host_enqueue_ms": round(host_ms, 3),
@@ -863,6 +936,8 @@ def main() -> None:
     ap.add_argument("--storage", default="shm", choices=["shm", "hugetmpfs"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c3ss", "c4", "c5"])
     ap.add_argument("--restore-gpus", type=int, default=None)
+    ap.add_argument("--save-mode", default="async", choices=["async", "sync"],
+                    help="async (default): each step's save is an async save + wait; sync: sync save")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--train-ms", type=float, default=1000.0)
     ap.add_argument("--inline-gc", action="store_true", help="c5: retention deletes inside wait() (reference)")

@@ -152,6 +152,15 @@ int tv_copy_boxes(int device, const tv_copy* copies, int n, void* stream);
 /* Bytes a box copy moves (sum of extents × itemsize) — for roofline accounting. */
 int64_t tv_copy_bytes(const tv_copy* copies, int n);
 
+/* Kernel timing (instrumentation for bench.py's roofline): while enabled, every box-copy
+ * or cast launch of the library — tv_copy_boxes and the engine's pack / unpack / fan-out
+ * launches — is bracketed by CUDA timing events on its own stream (the first recorded
+ * after the job-table upload, so the window is the kernel, not the host's enqueue).
+ * collect() waits for the recorded launches and returns their summed and longest
+ * durations, their algorithmic HBM bytes (read + write) and their count, then resets. */
+int tv_kernel_timing(int enable);
+int tv_kernel_timing_collect(double* ms_total, double* ms_max, int64_t* bytes, int64_t* launches);
+
 /* ---- engine ----------------------------------------------------------------------- */
 /* Pinned host slot ring (n_slots × slot_bytes), device staging of staging_bytes on each
  * device that touches it, and n_threads storage threads. */

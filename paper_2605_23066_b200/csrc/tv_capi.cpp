@@ -29,6 +29,8 @@ int engine_save(tv_engine*, const tv_write_item*, int, const tv_output*, int, tv
 int engine_load(tv_engine*, const tv_read_item*, int, const tv_input*, int, const tv_copy*, int,
                 tv_stats*);
 int copy_boxes(int, const tv_copy*, int, cudaStream_t);
+int kernel_timing(int);
+int kernel_timing_collect(double*, double*, int64_t*, int64_t*);
 
 }  // namespace tv
 
@@ -53,6 +55,14 @@ int tv_copy_boxes(int device, const tv_copy* copies, int n, void* stream) {
     return TV_ERR_ARG;
   }
   return tv::copy_boxes(device, copies, n, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tv_kernel_timing(int enable) { return tv::kernel_timing(enable); }
+
+int tv_kernel_timing_collect(double* ms_total, double* ms_max, int64_t* bytes,
+                             int64_t* launches) {
+  tv::DeviceGuard guard;
+  return tv::kernel_timing_collect(ms_total, ms_max, bytes, launches);
 }
 
 int64_t tv_copy_bytes(const tv_copy* copies, int n) {

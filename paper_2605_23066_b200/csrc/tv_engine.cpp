@@ -148,6 +148,87 @@ std::string parent_of(const std::string& path) {
   return p == std::string::npos ? std::string() : path.substr(0, p);
 }
 
+// ---- kernel timing (tv_kernel_timing) ---------------------------------------------------
+
+// Algorithmic HBM bytes of one launch: every byte copied is read once and written once;
+// a converting copy reads source elements and writes destination elements.
+int64_t job_traffic(const std::vector<CopyJob>& jobs) {
+  int64_t b = 0;
+  for (const auto& j : jobs) b += 2 * j.run * j.nruns;
+  return b;
+}
+int64_t job_traffic(const std::vector<CastJob>& jobs) {
+  int64_t b = 0;
+  for (const auto& j : jobs) b += j.run * j.nruns * (dtype_size(j.sdt) + dtype_size(j.ddt));
+  return b;
+}
+
+// While enabled, every box-copy / cast launch is bracketed by two timing events on its
+// stream: the first is recorded after the job-table upload, so the window is the kernel
+// (plus launch latency), not the host's enqueue work.  Collected (and reset) on demand.
+class KernelTimer {
+ public:
+  std::atomic<bool> on{false};
+  struct Rec {
+    int device;
+    cudaEvent_t a, b;
+    int64_t bytes;
+  };
+  cudaError_t begin(int device, cudaStream_t stream, cudaEvent_t* a) {
+    cudaError_t e = cudaEventCreate(a);
+    if (e == cudaSuccess) e = cudaEventRecord(*a, stream);
+    (void)device;
+    return e;
+  }
+  cudaError_t end(int device, cudaStream_t stream, cudaEvent_t a, int64_t bytes) {
+    cudaEvent_t b;
+    cudaError_t e = cudaEventCreate(&b);
+    if (e == cudaSuccess) e = cudaEventRecord(b, stream);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(m_);
+    recs_.push_back({device, a, b, bytes});
+    return cudaSuccess;
+  }
+  int collect(double* ms_total, double* ms_max, int64_t* bytes, int64_t* launches) {
+    std::vector<Rec> recs;
+    {
+      std::lock_guard<std::mutex> g(m_);
+      recs.swap(recs_);
+    }
+    double tot = 0, mx = 0;
+    int64_t by = 0;
+    int rc = TV_OK;
+    for (auto& r : recs) {
+      float ms = 0;
+      cudaSetDevice(r.device);
+      if (rc == TV_OK) {
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+        if (e != cudaSuccess) {
+          set_error(std::string("tv_kernel_timing_collect: ") + cudaGetErrorString(e));
+          rc = TV_ERR_CUDA;
+        }
+      }
+      tot += ms;
+      mx = std::max(mx, (double)ms);
+      by += r.bytes;
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    if (ms_total) *ms_total = tot;
+    if (ms_max) *ms_max = mx;
+    if (bytes) *bytes = by;
+    if (launches) *launches = (int64_t)recs.size();
+    return rc;
+  }
+
+ private:
+  std::mutex m_;
+  std::vector<Rec> recs_;
+};
+
+KernelTimer g_timer;
+
 // ---- per-device resources -------------------------------------------------------------
 
 // Uploads CopyJob tables to the device through a pinned ring; a region is reused only
@@ -207,8 +288,12 @@ class JobUploader {
     std::memcpy(host_ + head_, jobs.data(), bytes);
     TV_CUDA_CHECK(cudaMemcpyAsync(dev_ + head_, host_ + head_, bytes, cudaMemcpyHostToDevice,
                                   stream));
+    const bool timed = g_timer.on.load(std::memory_order_relaxed);
+    cudaEvent_t t0 = nullptr;
+    if (timed) TV_CUDA_CHECK(g_timer.begin(device_, stream, &t0));
     TV_CUDA_CHECK(launch(reinterpret_cast<const Job*>(dev_ + head_), (int)jobs.size(), total_units,
                          stream));
+    if (timed) TV_CUDA_CHECK(g_timer.end(device_, stream, t0, job_traffic(jobs)));
     cudaEvent_t ev;
     if (free_events_.empty()) {
       TV_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1205,6 +1290,15 @@ int engine_load(tv_engine* e, const tv_read_item* items, int n_items, const tv_i
   int rc = run.run();
   run.publish_stats();
   return rc;
+}
+
+int kernel_timing(int enable) {
+  g_timer.on.store(enable != 0);
+  return TV_OK;
+}
+
+int kernel_timing_collect(double* ms_total, double* ms_max, int64_t* bytes, int64_t* launches) {
+  return g_timer.collect(ms_total, ms_max, bytes, launches);
 }
 
 // Standalone batched copy (tv_copy_boxes): one launch on the caller's stream.

@@ -63,7 +63,8 @@ STATS = np.dtype(
 
 # Every symbol include/tvgpu.h declares (tests check the library exports all of them).
 EXPORTS = (
-    "tv_abi_version", "tv_last_error", "tv_copy_boxes", "tv_copy_bytes", "tv_engine_create",
+    "tv_abi_version", "tv_last_error", "tv_copy_boxes", "tv_copy_bytes", "tv_kernel_timing",
+    "tv_kernel_timing_collect", "tv_engine_create",
     "tv_engine_destroy", "tv_engine_save", "tv_engine_load", "tv_enable_peer_access",
     "tv_ipc_export", "tv_ipc_import", "tv_ipc_close", "tv_probe_storage", "tv_probe_pcie",
 )
@@ -79,6 +80,9 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tv_last_error": (I, [ctypes.c_char_p, ctypes.c_size_t]),
         "tv_copy_boxes": (I, [I, P, I, P]),
         "tv_copy_bytes": (L, [P, I]),
+        "tv_kernel_timing": (I, [I]),
+        "tv_kernel_timing_collect": (I, [ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(L),
+                                         ctypes.POINTER(L)]),
         "tv_engine_create": (I, [I, L, L, I, ctypes.POINTER(P)]),
         "tv_engine_destroy": (I, [P]),
         "tv_engine_save": (I, [P, P, I, P, I, P]),
@@ -230,6 +234,21 @@ def copy_boxes(device: int, copies: np.ndarray, stream: int = 0) -> None:
     check(lib().tv_copy_boxes(device, _ptr(copies), len(copies), stream), "tv_copy_boxes")
     with _totals_lock:
         TOTALS["kernels"]["kernel_launches"] += 1
+
+
+def kernel_timing(enable: bool) -> None:
+    """Bracket every later box-copy / cast launch with CUDA timing events (bench.py)."""
+    check(lib().tv_kernel_timing(1 if enable else 0), "tv_kernel_timing")
+
+
+def kernel_timing_collect() -> dict:
+    """Launches recorded since the last collect: summed / longest kernel ms, algorithmic
+    HBM bytes (read + write) and count.  Waits for the recorded launches."""
+    tot, mx = ctypes.c_double(), ctypes.c_double()
+    nbytes, n = ctypes.c_int64(), ctypes.c_int64()
+    check(lib().tv_kernel_timing_collect(ctypes.byref(tot), ctypes.byref(mx), ctypes.byref(nbytes),
+                                         ctypes.byref(n)), "tv_kernel_timing_collect")
+    return {"ms_total": tot.value, "ms_max": mx.value, "bytes": nbytes.value, "launches": n.value}
 
 
 def enable_peer_access(gpus: Sequence[int]) -> None:

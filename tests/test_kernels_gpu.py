@@ -119,3 +119,27 @@ def test_converting_copy_strided(src_dt, dst_dt):
     got = treemodel.DenseArray(dst_dt, dst[tuple(slice(o, o + e) for o, e in zip(doff, ext))].contiguous()).to_numpy()
     assert got.tobytes() == np.ascontiguousarray(expect).tobytes()
     assert int(flags.item()) == 0
+
+
+def test_kernel_timing_records_every_launch_with_algorithmic_bytes():
+    """tv_kernel_timing brackets each launch with events on its stream; bytes = 2 x copied."""
+    import torch
+
+    from paper_2605_23066_b200 import native
+
+    src = torch.randint(0, 100, (256, 1024), dtype=torch.int32, device="cuda")
+    dst = torch.zeros((128, 512), dtype=torch.int32, device="cuda")
+    native.kernel_timing_collect()  # drop anything recorded earlier
+    native.kernel_timing(True)
+    try:
+        for _ in range(3):
+            _copy(native, torch, src, (7, 100), dst, (0, 0), (128, 512), 4)
+    finally:
+        native.kernel_timing(False)
+    _copy(native, torch, src, (0, 0), dst, (0, 0), (128, 512), 4)  # not recorded
+    got = native.kernel_timing_collect()
+    assert got["launches"] == 3
+    assert got["bytes"] == 3 * 2 * 128 * 512 * 4
+    assert 0 < got["ms_max"] <= got["ms_total"]
+    assert torch.equal(dst, src[:128, :512])
+    assert native.kernel_timing_collect()["launches"] == 0
