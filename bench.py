@@ -440,6 +440,11 @@ def run_ours(args) -> dict:
         blocks.append(d.max(b_ms))
     native.kernel_timing(False)
     ktime = native.kernel_timing_collect()
+    from paper_2605_23066_b200 import timeline
+
+    me = d.rank if d.on else 0
+    phases = {"save": dict(timeline.LAST_SAVE.get(me, {})),
+              "restore": {**timeline.LAST_RESTORE.get(me, {}), **timeline.LAST_RESTORE.get(-1, {})}}
     after = native.totals()
     clock_info = clocks.stop() if d.rank == 0 else {}
     kernels = d.sum(after["kernel_launches"] - before["kernel_launches"])
@@ -531,6 +536,7 @@ def run_ours(args) -> dict:
         },
         "clocks": clock_info,
         "engine_rank0": engine,
+        "phases_ms_rank0_last_step": phases,
     }
     if d.rank == 0:
         pcie_d2h = probe["pcie_d2h_GBps_per_gpu"] * N
