@@ -759,6 +759,7 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     first_copy = np.zeros(len(items), np.int32)
     n_copies = np.zeros(len(items), np.int32)
     cols: dict[str, list] = {k: [] for k in ("sb", "ss", "so", "db", "ds", "do", "ext", "isz", "sdt", "ddt", "flg")}
+    peer_bytes = 0
     for j, it in enumerate(items):
         f = it.fetch
         fetched = tuple(zip(f.origin, f.shape))
@@ -788,6 +789,8 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
             cols["ds"].append(tuple(e for _, e in d.ranges))
             cols["do"].append(tuple(h - o for (h, _), (o, _) in zip(hit, d.ranges)))
             cols["ext"].append(tuple(e for _, e in hit))
+            if d.gpu != it.reader_gpu:  # lands in another GPU's HBM: NVLink (P2P / IPC)
+                peer_bytes += math.prod(e for _, e in hit) * d.itemsize
             cols["isz"].append(d.src_itemsize if d.src_code else d.itemsize)
             cols["sdt"].append(d.src_code)
             cols["ddt"].append(d.dst_code)
@@ -805,6 +808,7 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     cfg = engine_cfg or native.EngineConfig()
     with native.engine_lease(cfg, concurrent) as eng:
         stats = eng.load(ritems, inputs, copies)
+    native.account_peer(peer_bytes)
     backend.record_bulk(
         store.identity, [it.fetch.op for it in items], [it.fetch.key for it in items],
         [it.fetch.nbytes for it in items], [0] * len(items),

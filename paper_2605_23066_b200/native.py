@@ -206,7 +206,7 @@ def write_table(src_base, src_shape, src_off, ext, itemsize, file, device, file_
 _FIELDS = ("kernel_launches", "dma_copies", "bytes_device", "bytes_storage", "bytes_packed", "files",
            "seconds_total", "seconds_io", "seconds_wait_dma", "seconds_wait_slot")
 TOTALS = {"save": dict.fromkeys(_FIELDS, 0), "load": dict.fromkeys(_FIELDS, 0),
-          "kernels": {"kernel_launches": 0}}
+          "kernels": {"kernel_launches": 0}, "peer": {"bytes": 0}}
 _totals_lock = threading.Lock()
 
 
@@ -216,11 +216,18 @@ def _account(kind: str, stats) -> None:
             TOTALS[kind][k] += stats[k].item()
 
 
+def account_peer(nbytes: int) -> None:
+    """Restore bytes the fan-out kernel stored into another GPU's HBM (NVLink)."""
+    with _totals_lock:
+        TOTALS["peer"]["bytes"] += int(nbytes)
+
+
 def totals() -> dict:
     """Combined counters plus the per-kind ("save" / "load") breakdown."""
     with _totals_lock:
         out = {k: TOTALS["save"][k] + TOTALS["load"][k] for k in _FIELDS}
         out["kernel_launches"] += TOTALS["kernels"]["kernel_launches"]
+        out["peer_bytes"] = TOTALS["peer"]["bytes"]
         out["save"] = dict(TOTALS["save"])
         out["load"] = dict(TOTALS["load"])
         return out
