@@ -13,6 +13,6 @@ $K > gpurun_out/e_kb_snap.log 2>&1 && \
 echo "snap ncu rc=$?"; cat gpurun_out/e_kb_snap.log
 P="python tools/pcie_range_probe.py"
 $P > gpurun_out/e_pcie.log 2>&1 && \
-  ncu --replay-mode range --profile-from-start off --metrics pcie__read_bytes.sum,pcie__write_bytes.sum,gpu__time_duration.sum \
+  ncu --replay-mode range --metrics pcie__read_bytes.sum,pcie__write_bytes.sum,gpu__time_duration.sum \
     --csv --log-file gpurun_out/e_pcie_ncu.csv $P > gpurun_out/e_pcie_ncu.log 2>&1
 echo "pcie ncu rc=$?"; cat gpurun_out/e_pcie.log; cat gpurun_out/e_pcie_ncu.csv | tail -8
