@@ -503,7 +503,7 @@ def run_ours(args) -> dict:
     if d.rank == 0:
         shutil.rmtree(os.path.join(base, "bench"), ignore_errors=True)
 
-    kern = kernel_roofline(tv, native, state, rt, d, ksave, kload, args, step_ms)
+    kern = kernel_roofline(tv, native, state, rt, d, ksave, kload, args, step_ms, peer_gb)
     e2e = end_to_end(tv, rt, wl, args, d, base) if not args.no_e2e else None
 
     peaks = measured_peaks()
@@ -718,7 +718,8 @@ def _ncu_traffic(bytes_per_launch: int):
     return None, None
 
 
-def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, step_ms: float) -> dict:
+def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, step_ms: float,
+                    peer_gb: float = 0.0) -> dict:
     """The box-copy kernel inside the timed steps, timed live by libtvgpu with CUDA events on
     the launching stream (tv_kernel_timing); algorithmic bytes = 2 × bytes copied.  Save side
     (async mode): the device snapshot, ONE launch per GPU per step.  Restore side: unpack /
@@ -761,6 +762,17 @@ def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, st
     s_sum = summary(ksave, "box_copy_kernel (async-save device snapshot: this GPU's write ranges -> "
                            "arena, 1 launch per GPU per step)")
     l_sum = summary(kload, "box_copy_kernel (restore unpack / reshard fan-out into local and peer HBM)")
+    if l_sum is not None and peer_gb > 0:
+        # the fan-out's binding link: bytes stored into peer HBM leave each GPU over NVLink;
+        # per-GPU egress = peer bytes / (summed kernel time / GPUs), against the measured
+        # 770 GB/s peer-copy bandwidth per direction (B200_PROFILING.md)
+        n_gpus = d.world if d.on else max(1, args.restore_gpus or args.gpus)
+        per_gpu_s = d.sum(kload["ms_total"]) / 1e3 / n_gpus
+        nv = peer_gb / per_gpu_s / n_gpus
+        l_sum["nvlink"] = {"peer_GB_in_timed_steps": round(peer_gb, 3),
+                           "achieved_GBps_per_gpu": round(nv, 1), "peak_GBps_per_gpu": 770.0,
+                           "frac": round(nv / 770.0, 4),
+                           "peak_source": "B200_PROFILING.md measured peer copy, per direction"}
     live = [x for x in (s_sum, l_sum) if x is not None]
     if live:
         best = max(live, key=lambda x: x["ms_per_launch"] * x["launches_in_timed_region"])
