@@ -576,7 +576,7 @@ def run_ours(args) -> dict:
             **probe,
         }
         result["roofline"]["peak_source"] = peaks["source"]
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and N == 1:  # rank 0 at N=1 only (the contract)
             result["cpu_baseline"] = cpu_baseline(args, sample_layers=args.cpu_layers, root_dir=base)
     return result
 
