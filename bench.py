@@ -382,7 +382,9 @@ def run_ours(args) -> dict:
         acc["bytes"] += k["bytes"]
         acc["launches"] += k["launches"]
 
-    def step(i: int, opts=None):
+    verified = {}
+
+    def step(i: int, opts=None, verify: bool = False):
         """One save (call -> committed) + one restore (call -> every shard resident).
         Async mode (Orbax's default for training): the blocking device snapshot, then
         wait() for the background pack/D2H/write/commit.  Returns (save ms, restore ms,
@@ -412,6 +414,10 @@ def run_ours(args) -> dict:
         t2 = time.perf_counter()
         if timing:
             _add(kload, native.kernel_timing_collect())
+        if verify:  # outside every timed number: restored bytes == saved state, on device
+            nb, bad = verify_restore(tv, state, out)
+            verified["bytes_compared"] = int(d.sum(nb))
+            verified["mismatched_boxes"] = int(d.sum(bad))
         d.barrier()
         del out
         if d.rank == 0:
@@ -491,12 +497,12 @@ def run_ours(args) -> dict:
     # side, one extra save (untimed for `value`) in the other mode gives the other
     if args.save_mode == "async":
         blocking_ms = statistics.mean(blocks)
-        other = step(args.warmup + args.steps, sync_opts)
+        other = step(args.warmup + args.steps, sync_opts, verify=True)
         sync_save_ms = d.max(other[0])
         async_total_ms = save_ms
     else:
         sync_save_ms = save_ms
-        other = step(args.warmup + args.steps, async_opts)
+        other = step(args.warmup + args.steps, async_opts, verify=True)
         blocking_ms = d.max(other[4])
         async_total_ms = d.max(other[0])
     d.barrier()
@@ -554,6 +560,9 @@ def run_ours(args) -> dict:
         "clocks": clock_info,
         "engine_rank0": engine,
         "phases_ms_rank0_last_step": phases,
+        "restore_verified": dict(verified, how="after the timed steps: every restored shard's overlap "
+                                               "with every saved shard compared with torch.equal on "
+                                               "the device (all ranks)"),
         "reshard_exchange": {
             "nvlink_GB_per_restore": round(peer_gb / args.steps, 3),
             "nvlink_GBps_over_restore": round(peer_gb / args.steps / (restore_ms / 1e3), 2),
@@ -819,6 +828,44 @@ def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, st
         "host_enqueue_ms": round(host_ms, 3),
         "launches_in_timed_region": 0,
     }
+
+
+def verify_restore(tv, state, out) -> tuple[int, int]:
+    """Restored shards vs the saved state, byte for byte on the device: each target shard's
+    overlap with each addressable source shard must be equal (any target sharding).
+    Returns (bytes compared, mismatching boxes)."""
+    import torch
+
+    compared = bad = 0
+    for name, tree in out.items():
+        src = dict(tv.flatten(state[name]))
+        for path, leaf in tv.flatten(tree):
+            ref = src[path]
+            if not hasattr(leaf, "shards") or not hasattr(ref, "shards"):
+                continue
+            s_ranges, t_ranges = ref.shard_ranges(), leaf.shard_ranges()
+            for tdev, t in leaf.shards.items():
+                tr = t_ranges[tdev]
+                for sdev, sv in ref.shards.items():
+                    sr = s_ranges[sdev]
+                    hit = []
+                    for (a0, ae), (b0, be) in zip(tr, sr):
+                        lo, hi = max(a0, b0), min(a0 + ae, b0 + be)
+                        if hi <= lo:
+                            hit = None
+                            break
+                        hit.append((lo, hi - lo))
+                    if hit is None:
+                        continue
+                    a = t[tuple(slice(o - to, o - to + e) for (o, e), (to, _) in zip(hit, tr))]
+                    b = sv[tuple(slice(o - so, o - so + e) for (o, e), (so, _) in zip(hit, sr))]
+                    if b.device != a.device:
+                        b = b.to(a.device)
+                    ints = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
+                    a, b = a.view(ints[a.element_size()]), b.view(ints[b.element_size()])
+                    compared += a.numel() * a.element_size()
+                    bad += 0 if torch.equal(a, b) else 1  # bit patterns (NaN-safe)
+    return compared, bad
 
 
 def _device_tensors(leaf):
