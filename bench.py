@@ -549,11 +549,12 @@ def run_ours(args) -> dict:
         "io_roofline": None,
         "roofline": kern,
         "e2e": e2e,
-        "gpu_launches": int(kernels + dmas),
+        "gpu_launches": int(kernels),
         "gpu_launches_breakdown": {
             "box_copy_kernel": int(kernels),
             "copy_engine_dma_by_libtvgpu": int(dmas),
-            "note": "contiguous chunk payloads move by copy-engine DMA issued by libtvgpu's engine "
+            "note": "gpu_launches counts libtvgpu kernel launches only (summed over ranks); "
+                    "contiguous chunk payloads move by copy-engine DMA issued by libtvgpu's engine "
                     "(measured faster than SM-driven PCIe: profiles/r01_pcie_kernel_vs_ce.jsonl); "
                     "async-save snapshots, strided boxes and reshard scatters run box_copy_kernel",
         },
