@@ -943,7 +943,8 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
 # -- CPU baseline: the oracle port of the reference ------------------------------------------------
 
 
-def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_dir: str | None = None) -> dict:
+def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_dir: str | None = None,
+                 steps: int = 1, warmup: int = 0) -> dict:
     """The reference's save + restore (oracle/treevault_oracle.py restating
     save_pipeline/chunkstore/load_pipeline) on a bounded sample of the workload, one host
     thread per simulated process, same directory type as the GPU run."""
@@ -974,24 +975,30 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
         specs["state"][f"{t}/{p}"] = ([("fsdp", P)], P, None, ("fsdp",) + (None,) * (len(shape) - 1))
     sample_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
     root = os.path.join(root_dir or args.dir, "cpu_baseline")
+    saves, restores = [], []
+    for i in range(warmup + steps):
+        shutil.rmtree(root, ignore_errors=True)
+        os.makedirs(root)
+        t0 = time.perf_counter()
+        files = orc.expected_checkpoint(tree, specs, {}, P, "fs", path="ck")
+        keys = sorted(files)
+        per = [dict((k, files[k]) for k in keys[j::P]) for j in range(P)]
+        ths = [threading.Thread(target=orc.save_to_directory, args=(root, part)) for part in per]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        t_save = time.perf_counter() - t0
+        del files, per
+        t0 = time.perf_counter()
+        restored = orc.restore_from_directory(root, "ck", P)
+        t_restore = time.perf_counter() - t0
+        del restored
+        if i >= warmup:
+            saves.append(t_save)
+            restores.append(t_restore)
     shutil.rmtree(root, ignore_errors=True)
-    os.makedirs(root)
-    t0 = time.perf_counter()
-    files = orc.expected_checkpoint(tree, specs, {}, P, "fs", path="ck")
-    keys = sorted(files)
-    per = [dict((k, files[k]) for k in keys[i::P]) for i in range(P)]
-    ths = [threading.Thread(target=orc.save_to_directory, args=(root, part)) for part in per]
-    for th in ths:
-        th.start()
-    for th in ths:
-        th.join()
-    t_save = time.perf_counter() - t0
-    del files, per
-    t0 = time.perf_counter()
-    restored = orc.restore_from_directory(root, "ck", P)
-    t_restore = time.perf_counter() - t0
-    del restored
-    shutil.rmtree(root, ignore_errors=True)
+    t_save, t_restore = statistics.mean(saves), statistics.mean(restores)
     value = 2 * sample_bytes / (t_save + t_restore) / 1e9
     return {
         "value": round(value, 3),
@@ -999,26 +1006,37 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
         "cores": P,
         "kind": "port",
         "sample": f"{sample_layers} transformer layers of the C2 tree (no embed/lm_head), "
-                  f"{sample_bytes} bytes, FSDP-{P} over {P} simulated processes",
+                  f"{sample_bytes} bytes, FSDP-{P} over {P} simulated processes (one host thread "
+                  f"each), save + restore per step, mean of {steps} after {warmup} warm-up",
         "save_GBps": round(sample_bytes / t_save / 1e9, 3),
         "restore_GBps": round(sample_bytes / t_restore / 1e9, 3),
     }
 
 
 def run_reference(args) -> dict:
+    """The reference arm: the reference's CPU algorithm (the oracle port; the reference is
+    Python and cannot travel to the GPU box) on the box's host cores, --warmup W + --steps K
+    save+restore steps of a bounded sample of the same C2 workload, same storage target."""
     d = Dist()
     res = cpu_baseline(args, sample_layers=args.cpu_layers,
-                       root_dir=prepare_storage(args, d) if args.storage != "shm" else None)
+                       root_dir=prepare_storage(args, d) if args.storage != "shm" else None,
+                       steps=args.steps, warmup=args.warmup)
+    N = d.world if d.on else args.gpus
     return {
         "impl": "reference",
         "metric": "checkpoint save+restore throughput (GB/s of tree bytes, save and restore each count once)",
         "value": res["value"],
         "unit": "GB/s",
-        "n_gpus": d.world if d.on else args.gpus,
-        "steps": 1,
-        "warmup": 0,
+        "n_gpus": N,
+        "steps": args.steps,
+        "warmup": args.warmup,
         "higher_is_better": True,
-        "config": {"workload": res["sample"]},
+        "dtype": "bf16+f32 bytes (pure data movement)",
+        "data": "synthetic (numpy RNG, Llama-3-8B shapes)",
+        "config": {"workload": f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu (bounded sample: {res['sample']})",
+                   "config": "c2", "storage": f"oracle port writing/reading {args.dir} (tmpfs)"},
+        "save_GBps": res["save_GBps"],
+        "restore_GBps": res["restore_GBps"],
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
