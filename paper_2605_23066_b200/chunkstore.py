@@ -18,6 +18,7 @@ documents are host logic mirroring ``chunkstore.py:50-246, 249-305, 426-454, 603
 
 from __future__ import annotations
 
+import bisect
 import itertools
 import math
 from bisect import bisect_left
@@ -219,6 +220,54 @@ def _strides(shape: tuple[int, ...]) -> tuple[int, ...]:
     for d in range(len(shape) - 2, -1, -1):
         out[d] = out[d + 1] * shape[d + 1]
     return tuple(out)
+
+
+class BoxIndex:
+    """Which of a set of boxes meet a query box, without testing every box.
+
+    Target shardings are grids (mesh axes split dimensions), so per dimension the boxes'
+    intervals are either identical or disjoint: a query is answered by a bisection per
+    dimension and a lookup of the product of the intervals it meets.  Any other set of
+    boxes falls back to the linear scan.  Results keep the input order."""
+
+    def __init__(self, boxes: Sequence[tuple[Range, ...]]):
+        self.boxes = [tuple(b) for b in boxes]
+        self.by_box: dict[tuple[Range, ...], list[int]] = {}
+        for i, b in enumerate(self.boxes):
+            self.by_box.setdefault(b, []).append(i)
+        rank = len(self.boxes[0]) if self.boxes else 0
+        self.dims: list[list[Range]] | None = []
+        for d in range(rank):
+            iv = sorted({b[d] for b in self.boxes})
+            if any(o1 + e1 > o2 for (o1, e1), (o2, _) in zip(iv, iv[1:])):
+                self.dims = None  # overlapping intervals: not a grid
+                break
+            self.dims.append(iv)
+        if self.dims is not None and math.prod(len(iv) for iv in self.dims) != len(self.by_box):
+            self.dims = None      # not every product cell is a box: not a full grid
+
+    def hits(self, box: tuple[Range, ...]) -> list[int]:
+        if self.dims is None:
+            return [i for i, b in enumerate(self.boxes) if _intersect(box, b) is not None]
+        per_dim = []
+        for (bo, be), iv in zip(box, self.dims):
+            lo = bisect.bisect_right(iv, (bo, math.inf)) - 1
+            lo = max(lo, 0)
+            sel = []
+            for j in range(lo, len(iv)):
+                o, e = iv[j]
+                if o >= bo + be:
+                    break
+                if o + e > bo and e > 0 and be > 0:
+                    sel.append(iv[j])
+            if not sel:
+                return []
+            per_dim.append(sel)
+        out: list[int] = []
+        for cell in itertools.product(*per_dim):
+            out.extend(self.by_box.get(cell, ()))
+        out.sort()
+        return out
 
 
 def box_is_contiguous(shape: Sequence[int], off: Sequence[int], ext: Sequence[int]) -> bool:
@@ -590,12 +639,18 @@ def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMet
     n_subs = math.prod(subs_per)
     contiguous = _slab_is_contiguous(r, w)
     wstrides = _strides(w)
-    chunks: dict[tuple[int, ...], set[tuple[int, ...]]] = {}
+    chunks: dict[tuple[int, ...], set[tuple[int, ...]] | None] = {}
     order: list[tuple[int, ...]] = []
-    for ranges in requests:
+    whole_only = n_subs == 1  # read chunk == write chunk: every covering chunk is read whole
+    for ranges in dict.fromkeys(tuple(r_) for r_ in requests):  # replicas ask for the same box
         if any(e == 0 for _, e in ranges):
             continue
         for coords in _covering(ranges, w):
+            if whole_only:
+                if coords not in chunks:
+                    chunks[coords] = None
+                    order.append(coords)
+                continue
             hit = _intersect(ranges, _cell_ranges(coords, w))
             if hit is None:
                 continue
@@ -621,7 +676,7 @@ def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMet
             base, op, whole = 0, "get", True
         needed = chunks[coords]
         origin = tuple(c * wi for c, wi in zip(coords, w))
-        if len(needed) == n_subs or not contiguous:
+        if whole_only or len(needed) == n_subs or not contiguous:
             out.append(Fetch(key, op, base, chunk_bytes, origin, tuple(w), whole))
             continue
         for sub in sorted(needed):

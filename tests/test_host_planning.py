@@ -173,3 +173,44 @@ def test_fs_listing_matches_full_walk(tmp_path):
     everything = sorted(k for k in backend._list(""))
     for prefix in ["", "a/", "a/ck/", "a/ck", "a/c", "b", "zz/", "a/ck/y/"]:
         assert backend._list(prefix) == [k for k in everything if k.startswith(prefix)], prefix
+
+
+def test_box_index_matches_linear_scan():
+    """BoxIndex (bisection on grid shardings) returns exactly the linear scan's hits, in
+    input order, for mesh shardings (replicas included) and for arbitrary box sets."""
+    import random
+
+    from paper_2605_23066_b200 import chunkstore as cs
+    from paper_2605_23066_b200.sharding import Mesh, PartitionSpec, Sharding, shards_of
+
+    rng = random.Random(5)
+    for case in range(300):
+        rank = rng.randint(1, 3)
+        shape = tuple(rng.choice([4, 8, 12, 16]) for _ in range(rank))
+        if case % 3 == 2:  # arbitrary, possibly overlapping boxes
+            boxes = []
+            for _ in range(rng.randint(1, 6)):
+                b = []
+                for g in shape:
+                    o = rng.randint(0, g - 1)
+                    b.append((o, rng.randint(1, g - o)))
+                boxes.append(tuple(b))
+        else:
+            axes = [("a", rng.choice([1, 2])), ("b", rng.choice([1, 2, 4]))]
+            mesh = Mesh.create(axes, process_count=1)
+            names = [None, "a", "b"]
+            spec = [rng.choice(names) for _ in range(rank)]
+            used = [n for n in spec if n]
+            if len(used) != len(set(used)) or any(
+                    g % dict(axes)[n] for g, n in zip(shape, spec) if n):
+                continue
+            boxes = [sh.ranges for sh in shards_of(Sharding(mesh, PartitionSpec.of(*spec), shape))]
+        index = cs.BoxIndex(boxes)
+        for _ in range(10):
+            q = []
+            for g in shape:
+                o = rng.randint(0, g - 1)
+                q.append((o, rng.randint(1, g - o)))
+            q = tuple(q)
+            expect = [i for i, b in enumerate(boxes) if cs._intersect(q, b) is not None]
+            assert index.hits(q) == expect, (boxes, q)
