@@ -19,6 +19,7 @@ documents are host logic mirroring ``chunkstore.py:50-246, 249-305, 426-454, 603
 from __future__ import annotations
 
 import bisect
+import functools
 import itertools
 import math
 from bisect import bisect_left
@@ -122,12 +123,16 @@ class ArrayStorageMetadata:
     @classmethod
     def from_json(cls, doc: dict) -> "ArrayStorageMetadata":
         try:
-            return cls(
-                tuple(doc["global_shape"]), doc["dtype"], tuple(doc["shard_shape"]),
-                tuple(doc["write_chunk"]), tuple(doc["read_chunk"]), doc["layout"],
-            )
+            key = (tuple(doc["global_shape"]), doc["dtype"], tuple(doc["shard_shape"]),
+                   tuple(doc["write_chunk"]), tuple(doc["read_chunk"]), doc["layout"])
+            return _storage_meta_of(*key)  # leaves share a handful of distinct entries
         except (KeyError, TypeError) as exc:
             raise CorruptionError(f"malformed array metadata: {exc}") from exc
+
+
+@functools.lru_cache(maxsize=1 << 14)
+def _storage_meta_of(*key) -> ArrayStorageMetadata:
+    return ArrayStorageMetadata(*key)
 
 
 def _grid_consistent(global_shape: tuple[int, ...], part: tuple[int, ...]) -> bool:
