@@ -1,6 +1,7 @@
 #!/bin/bash
 # slot-ring sizing on a huge-page tmpfs (PCIe-bound there), full C2, 1 GPU
 cd "$(dirname "$0")/.."
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/hs_gpu_tests.log 2>&1; tail -2 gpurun_out/hs_gpu_tests.log
 M=/mnt/tvsweep_huge; mkdir -p $M
 KB=$(awk '/MemTotal/{print int($2*0.8)}' /proc/meminfo)
 mount -t tmpfs -o size=${KB}k,huge=always tmpfs $M || exit 3
