@@ -255,38 +255,46 @@ __device__ __forceinline__ void cast_job(const CastJob& j, int64_t local, uint32
   else cast_flat<S, D>(j, local, bad);
 }
 
-template <typename S>
-__device__ __forceinline__ void cast_dst(const CastJob& j, int64_t local, uint32_t& bad) {
-  switch (j.ddt) {
-    case TV_DT_F32: cast_job<S, float>(j, local, bad); break;
-    case TV_DT_F64: cast_job<S, double>(j, local, bad); break;
-    case TV_DT_BF16: cast_job<S, BF16>(j, local, bad); break;
-    case TV_DT_I32: cast_job<S, int32_t>(j, local, bad); break;
-    case TV_DT_I64: cast_job<S, long long>(j, local, bad); break;
-    case TV_DT_U8: cast_job<S, uint8_t>(j, local, bad); break;
-    default: break;
-  }
-}
-
+// One kernel per (source, destination) dtype pair: each instantiation holds only its own
+// conversion path, so its register allocation (and occupancy) is that path's, not the
+// worst case over every pair.  A batch is grouped by pair on the host.
+template <typename S, typename D>
 __global__ void __launch_bounds__(kThreads) box_cast_kernel(const CastJob* __restrict__ jobs,
                                                             int n_jobs, int64_t block0) {
   const int64_t block = block0 + blockIdx.x;
   const CastJob j = jobs[find_cast_job(jobs, n_jobs, block)];
   const int64_t local = block - j.unit_begin;
   uint32_t bad = 0;
-  if (local < j.units) {
-    switch (j.sdt) {
-      case TV_DT_F32: cast_dst<float>(j, local, bad); break;
-      case TV_DT_F64: cast_dst<double>(j, local, bad); break;
-      case TV_DT_BF16: cast_dst<BF16>(j, local, bad); break;
-      case TV_DT_I32: cast_dst<int32_t>(j, local, bad); break;
-      case TV_DT_I64: cast_dst<long long>(j, local, bad); break;
-      case TV_DT_U8: cast_dst<uint8_t>(j, local, bad); break;
-      default: break;
-    }
-  }
+  if (local < j.units) cast_job<S, D>(j, local, bad);
   bad = __reduce_or_sync(0xffffffffu, bad);
   if (bad && (threadIdx.x & 31) == 0) atomicOr(j.flags, bad);
+}
+
+using CastKernel = void (*)(const CastJob*, int, int64_t);
+
+template <typename S>
+CastKernel pick_dst(int ddt) {
+  switch (ddt) {
+    case TV_DT_F32: return box_cast_kernel<S, float>;
+    case TV_DT_F64: return box_cast_kernel<S, double>;
+    case TV_DT_BF16: return box_cast_kernel<S, BF16>;
+    case TV_DT_I32: return box_cast_kernel<S, int32_t>;
+    case TV_DT_I64: return box_cast_kernel<S, long long>;
+    case TV_DT_U8: return box_cast_kernel<S, uint8_t>;
+    default: return nullptr;
+  }
+}
+
+CastKernel pick_kernel(int sdt, int ddt) {
+  switch (sdt) {
+    case TV_DT_F32: return pick_dst<float>(ddt);
+    case TV_DT_F64: return pick_dst<double>(ddt);
+    case TV_DT_BF16: return pick_dst<BF16>(ddt);
+    case TV_DT_I32: return pick_dst<int32_t>(ddt);
+    case TV_DT_I64: return pick_dst<long long>(ddt);
+    case TV_DT_U8: return pick_dst<uint8_t>(ddt);
+    default: return nullptr;
+  }
 }
 
 }  // namespace
@@ -382,28 +390,45 @@ bool normalize_cast(const tv_copy& c, std::vector<CastJob>& out, std::string& er
 }
 
 int64_t plan_cast_units(std::vector<CastJob>& jobs) {
-  int64_t total = 0;
-  for (auto& j : jobs) {
+  // Group by dtype pair (one kernel each); units are numbered within each group.
+  std::stable_sort(jobs.begin(), jobs.end(), [](const CastJob& a, const CastJob& b) {
+    return a.sdt != b.sdt ? a.sdt < b.sdt : a.ddt < b.ddt;
+  });
+  int64_t total = 0, group = 0;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    auto& j = jobs[i];
+    if (i > 0 && (j.sdt != jobs[i - 1].sdt || j.ddt != jobs[i - 1].ddt)) group = 0;
     if (j.mode == 0) {
       const int64_t segs = (j.run + kSegV - 1) / kSegV;
       j.units = (j.nruns * segs + kWarps - 1) / kWarps;
     } else {
       j.units = (j.nruns * j.run + kFlat - 1) / kFlat;
     }
-    j.unit_begin = total;
+    j.unit_begin = group;
+    group += j.units;
     total += j.units;
   }
   return total;
 }
 
-cudaError_t launch_cast_jobs(const CastJob* dev_jobs, int n_jobs, int64_t total_units,
-                             cudaStream_t stream) {
+cudaError_t launch_cast_jobs(const CastJob* dev_jobs, const CastJob* host_jobs, int n_jobs,
+                             int64_t, cudaStream_t stream) {
   const int64_t max_grid = 0x7fffffffLL;
-  for (int64_t b0 = 0; b0 < total_units; b0 += max_grid) {
-    const unsigned grid = (unsigned)std::min<int64_t>(max_grid, total_units - b0);
-    box_cast_kernel<<<grid, kThreads, 0, stream>>>(dev_jobs, n_jobs, b0);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+  for (int g0 = 0; g0 < n_jobs;) {
+    int g1 = g0 + 1;
+    while (g1 < n_jobs && host_jobs[g1].sdt == host_jobs[g0].sdt &&
+           host_jobs[g1].ddt == host_jobs[g0].ddt)
+      ++g1;
+    const CastKernel k = pick_kernel(host_jobs[g0].sdt, host_jobs[g0].ddt);
+    if (!k) return cudaErrorInvalidValue;
+    const int64_t units = host_jobs[g1 - 1].unit_begin + host_jobs[g1 - 1].units;
+    for (int64_t b0 = 0; b0 < units; b0 += max_grid) {
+      const unsigned grid = (unsigned)std::min<int64_t>(max_grid, units - b0);
+      k<<<grid, kThreads, 0, stream>>>(dev_jobs + g0, g1 - g0, b0);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    g0 = g1;
   }
   return cudaSuccess;
 }

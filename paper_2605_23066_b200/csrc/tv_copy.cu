@@ -300,8 +300,8 @@ int64_t plan_units(std::vector<CopyJob>& jobs) {
   return total;
 }
 
-cudaError_t launch_copy_jobs(const CopyJob* dev_jobs, int n_jobs, int64_t total_units,
-                             cudaStream_t stream) {
+cudaError_t launch_copy_jobs(const CopyJob* dev_jobs, const CopyJob*, int n_jobs,
+                             int64_t total_units, cudaStream_t stream) {
   const int64_t max_grid = 0x7fffffffLL;
   for (int64_t b0 = 0; b0 < total_units; b0 += max_grid) {
     const unsigned grid = (unsigned)std::min<int64_t>(max_grid, total_units - b0);

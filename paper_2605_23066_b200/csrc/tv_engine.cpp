@@ -291,8 +291,8 @@ class JobUploader {
     const bool timed = g_timer.on.load(std::memory_order_relaxed);
     cudaEvent_t t0 = nullptr;
     if (timed) TV_CUDA_CHECK(g_timer.begin(device_, stream, &t0));
-    TV_CUDA_CHECK(launch(reinterpret_cast<const Job*>(dev_ + head_), (int)jobs.size(), total_units,
-                         stream));
+    TV_CUDA_CHECK(launch(reinterpret_cast<const Job*>(dev_ + head_), jobs.data(), (int)jobs.size(),
+                         total_units, stream));
     if (timed) TV_CUDA_CHECK(g_timer.end(device_, stream, t0, job_traffic(jobs)));
     cudaEvent_t ev;
     if (free_events_.empty()) {

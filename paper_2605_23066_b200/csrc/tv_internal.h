@@ -60,8 +60,8 @@ bool normalize(const tv_copy& c, std::vector<CopyJob>& out, std::string& err);
 // Assign units/unit_begin and launch the batched copy kernel on `stream`.
 // `dev_jobs` must point to device-visible memory holding `jobs` (the caller stages it).
 int64_t plan_units(std::vector<CopyJob>& jobs);
-cudaError_t launch_copy_jobs(const CopyJob* dev_jobs, int n_jobs, int64_t total_units,
-                             cudaStream_t stream);
+cudaError_t launch_copy_jobs(const CopyJob* dev_jobs, const CopyJob* host_jobs, int n_jobs,
+                             int64_t total_units, cudaStream_t stream);
 
 // Converting copy (load-time cast fused into the unpack): like CopyJob but in elements,
 // with different element sizes on both sides.
@@ -86,8 +86,10 @@ bool is_cast(const tv_copy& c);
 int dtype_size(int dt);
 bool normalize_cast(const tv_copy& c, std::vector<CastJob>& out, std::string& err);
 int64_t plan_cast_units(std::vector<CastJob>& jobs);
-cudaError_t launch_cast_jobs(const CastJob* dev_jobs, int n_jobs, int64_t total_units,
-                             cudaStream_t stream);
+// Jobs are grouped by dtype pair by plan_cast_units (unit_begin restarts per group);
+// one launch per group of the pair's specialised kernel.
+cudaError_t launch_cast_jobs(const CastJob* dev_jobs, const CastJob* host_jobs, int n_jobs,
+                             int64_t total_units, cudaStream_t stream);
 
 // Is the box a single contiguous byte range of its array?  Sets byte offset/length.
 bool box_contiguous(const tv_array_box& b, const int64_t* ext, int rank, int itemsize,
