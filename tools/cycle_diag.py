@@ -1,6 +1,6 @@
 import gc, os, sys, shutil, collections
 sys.path.insert(0, os.getcwd())
-import torch
+import torch  # noqa: F401  (CUDA context before the package)
 import bench
 import paper_2605_23066_b200 as tv
 base = "/dev/shm/tvcyc"; shutil.rmtree(base, ignore_errors=True)

@@ -16,7 +16,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import statistics
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -25,7 +24,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2605_23066_b200 import chunkstore, native  # noqa: E402
+from paper_2605_23066_b200 import native  # noqa: E402
 
 D, FFN, V, KV = 4096, 14336, 128256, 1024
 
