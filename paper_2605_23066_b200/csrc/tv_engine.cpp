@@ -29,6 +29,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -417,11 +418,21 @@ class StagingPool {
   std::deque<Pending> pending_;
 };
 
+// DMA/kernel streams per device.  Work that must stay ordered (a slot's pack kernel and
+// its D2H; an item's H2D pieces and its unpack) always goes to one stream, chosen by the
+// slot / item index, so several copy engines can move independent slots at once.
+int dma_streams() {
+  const char* v = std::getenv("TVGPU_DMA_STREAMS");
+  const int n = v ? std::atoi(v) : 1;
+  return std::max(1, std::min(n, 16));
+}
+
 struct DeviceCtx {
   int device = -1;
-  cudaStream_t stream = nullptr;
+  std::vector<cudaStream_t> streams;
   std::unique_ptr<JobUploader> uploader;
   std::unique_ptr<StagingPool> staging;
+  cudaStream_t stream_for(int64_t k) const { return streams[(size_t)(k % (int64_t)streams.size())]; }
 };
 
 }  // namespace
@@ -448,7 +459,8 @@ int device_ctx(tv_engine* e, int device, DeviceCtx** out) {
     auto ctx = std::make_unique<DeviceCtx>();
     ctx->device = device;
     TV_CUDA_CHECK(cudaSetDevice(device));
-    TV_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->streams.resize(dma_streams());
+    for (auto& st : ctx->streams) TV_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     ctx->uploader = std::make_unique<JobUploader>(device);
     ctx->staging = std::make_unique<StagingPool>(device, e->staging_bytes);
     int rc = ctx->staging->init();
@@ -750,6 +762,7 @@ class SaveRun {
       return false;
     }
     char* host = e_->slots[s.index];
+    cudaStream_t stream = ctx->stream_for(s.index);
     if (!s.packs.empty()) {
       if (ctx->staging->capacity() < (int64_t)e_->n_slots * e_->slot_bytes) {
         err_.set(TV_ERR_NOMEM, "device staging smaller than n_slots*slot_bytes");
@@ -767,7 +780,7 @@ class SaveRun {
         stats_bytes_packed_ += box_bytes(s.packs[k].ext, s.packs[k].rank, s.packs[k].itemsize);
       }
       int64_t launches = 0;
-      rc = ctx->uploader->run(jobs, ctx->stream, &launches);
+      rc = ctx->uploader->run(jobs, stream, &launches);
       if (rc != TV_OK) {
         err_.set(rc, get_error());
         return false;
@@ -787,7 +800,7 @@ class SaveRun {
       }
     }
     for (auto& d : s.d2h) {
-      if (cudaMemcpyAsync(host + d.slot_off, d.src, d.n, cudaMemcpyDeviceToHost, ctx->stream) !=
+      if (cudaMemcpyAsync(host + d.slot_off, d.src, d.n, cudaMemcpyDeviceToHost, stream) !=
           cudaSuccess) {
         err_.set(TV_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(cudaGetLastError()));
         return false;
@@ -797,7 +810,7 @@ class SaveRun {
     }
     cudaEvent_t ev;
     if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventRecord(ev, ctx->stream) != cudaSuccess) {
+        cudaEventRecord(ev, stream) != cudaSuccess) {
       err_.set(TV_ERR_CUDA, "event record failed");
       return false;
     }
@@ -1011,8 +1024,10 @@ class LoadRun {
     // Drain all devices used.
     for (auto& kv : used_devices_) {
       cudaSetDevice(kv.first);
-      cudaError_t ce = cudaStreamSynchronize(kv.second->stream);
-      if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("restore stream: ") + cudaGetErrorString(ce));
+      for (cudaStream_t st : kv.second->streams) {
+        cudaError_t ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("restore stream: ") + cudaGetErrorString(ce));
+      }
     }
     for (int s = 0; s < e_->n_slots; ++s)
       if (slot_events_[s]) cudaEventDestroy(slot_events_[s]);
@@ -1147,7 +1162,8 @@ class LoadRun {
     DeviceCtx* ctx = ctx_for(it.device);
     if (!ctx) return false;
     cudaSetDevice(it.device);
-    if (cudaMemcpyAsync(st.base + t.off, host, t.n, cudaMemcpyHostToDevice, ctx->stream) !=
+    cudaStream_t stream = ctx->stream_for(t.item);  // every piece of an item: one stream
+    if (cudaMemcpyAsync(st.base + t.off, host, t.n, cudaMemcpyHostToDevice, stream) !=
         cudaSuccess) {
       err_.set(TV_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(cudaGetLastError()));
       return false;
@@ -1163,7 +1179,7 @@ class LoadRun {
       cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
       slot_event_dev_[t.slot] = it.device;
     }
-    cudaEventRecord(ev, ctx->stream);
+    cudaEventRecord(ev, stream);
     free_slots_.push(t.slot);
     if (st.left.fetch_sub(1) == 1) launch_copies(t.item);
     return true;
@@ -1175,6 +1191,7 @@ class LoadRun {
     DeviceCtx* ctx = ctx_for(it.device);
     if (!ctx) return;
     cudaSetDevice(it.device);
+    cudaStream_t stream = ctx->stream_for(item);  // after this item's H2D pieces
     if (it.n_copies > 0) {
       std::vector<CopyJob> jobs;
       std::vector<CastJob> casts;
@@ -1190,8 +1207,8 @@ class LoadRun {
         bytes_packed_ += box_bytes(cp.ext, cp.rank, cp.itemsize);
       }
       int64_t launches = 0;
-      int rc = ctx->uploader->run(jobs, ctx->stream, &launches);
-      if (rc == TV_OK) rc = ctx->uploader->run_cast(casts, ctx->stream, &launches);
+      int rc = ctx->uploader->run(jobs, stream, &launches);
+      if (rc == TV_OK) rc = ctx->uploader->run_cast(casts, stream, &launches);
       if (rc != TV_OK) {
         err_.set(rc, get_error());
         return;
@@ -1201,7 +1218,7 @@ class LoadRun {
     if (st.staged_off >= 0) {
       cudaEvent_t ev;
       cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      cudaEventRecord(ev, ctx->stream);
+      cudaEventRecord(ev, stream);
       ctx->staging->free_after(st.staged_off, it.nbytes, ev);
     }
   }
@@ -1260,10 +1277,10 @@ int engine_destroy(tv_engine* e) {
     std::lock_guard<std::mutex> g(e->dev_m);
     for (auto& kv : e->devices) {
       cudaSetDevice(kv.first);
-      cudaStreamSynchronize(kv.second->stream);
+      for (cudaStream_t st : kv.second->streams) cudaStreamSynchronize(st);
       kv.second->uploader.reset();
       kv.second->staging.reset();
-      cudaStreamDestroy(kv.second->stream);
+      for (cudaStream_t st : kv.second->streams) cudaStreamDestroy(st);
     }
     e->devices.clear();
   }
