@@ -388,10 +388,11 @@ class EngineConfig:
                threads runtime's processes, or torchrun's LOCAL_WORLD_SIZE ranks), minus
                one core per engine for its producer;
     n_slots  — 2 pinned slots per storage thread (fewer starves the readers);
-    slot     — 2 MiB, or 1 MiB when the rings of all engines would not fit the host's
-               last-level cache: the DMA'd bytes are re-read by pwrite / the H2D straight
-               from the LLC (DDIO).  Measured best on these boxes
-               (profiles/r01_engine_sweep_*.jsonl).
+    slot     — 4 MiB for a single engine (fewer, larger DMAs); with several engines
+               2 MiB, or 1 MiB when the rings of all engines would not fit the host's
+               last-level cache (the DMA'd bytes are re-read by pwrite / the H2D from the
+               LLC).  Measured best on these boxes (profiles/r01_engine_sweep_*.jsonl,
+               r01_ab_slot_*.txt: at 4 engines 1 MiB > 2 MiB > 4 MiB).
     """
 
     def __init__(self, slot_bytes: int | None = None, n_slots: int | None = None,
@@ -419,9 +420,15 @@ class EngineConfig:
         n_slots = self._n_slots or max(16, 2 * threads)
         slot = self._slot_bytes
         if slot is None:
-            llc = _llc_bytes()
-            ring_all = (2 << 20) * n_slots * self._engines(concurrent)
-            slot = (2 << 20) if (llc == 0 or ring_all <= 1.25 * llc) else (1 << 20)
+            engines = self._engines(concurrent)
+            if engines == 1:
+                # one engine owns the host: fewer, larger DMAs (measured +9 % restore on a
+                # huge-page tmpfs, neutral on /dev/shm: profiles/r01_ab_slot_2m_vs_4m_*.txt)
+                slot = 4 << 20
+            else:
+                llc = _llc_bytes()
+                ring_all = (2 << 20) * n_slots * engines
+                slot = (2 << 20) if (llc == 0 or ring_all <= 1.25 * llc) else (1 << 20)
         staging = self._staging or max(n_slots * slot, 1 << 30)
         return n_slots, slot, staging, threads
 
