@@ -458,6 +458,20 @@ def run_ours(args) -> dict:
     clocks = ClockSampler()
     if d.rank == 0:
         clocks.start()
+    import gc
+
+    gc_ms = [0.0, 0, 0]  # time, collections, gen-2 collections in the timed steps (this rank)
+    gc_t0 = [0.0]
+
+    def _gc_cb(phase, info):
+        if phase == "start":
+            gc_t0[0] = time.perf_counter()
+        else:
+            gc_ms[0] += (time.perf_counter() - gc_t0[0]) * 1e3
+            gc_ms[1] += 1
+            gc_ms[2] += int(info.get("generation") == 2)
+
+    gc.callbacks.append(_gc_cb)
     before = native.totals()
     native.kernel_timing(True)
     timing = True
@@ -471,6 +485,7 @@ def run_ours(args) -> dict:
     native.kernel_timing(False)
     timing = False
     native.kernel_timing_collect()
+    gc.callbacks.remove(_gc_cb)
     from paper_2605_23066_b200 import timeline
 
     me = d.rank if d.on else 0
@@ -570,6 +585,8 @@ def run_ours(args) -> dict:
         "clocks": clock_info,
         "engine_rank0": engine,
         "phases_ms_rank0_last_step": phases,
+        "python_gc_rank0": {"ms_per_step": round(gc_ms[0] / args.steps, 2),
+                            "collections": gc_ms[1], "gen2": gc_ms[2]},
         "restore_verified": dict(verified, how="after the timed steps: every restored shard's overlap "
                                                "with every saved shard compared with torch.equal on "
                                                "the device (all ranks)"),

@@ -131,6 +131,47 @@ def datapath(base: str) -> None:
         assert sorted(node.shards) == [rt.rank], node.shards.keys()
         got = tv.DenseArray(leaf[1], node.shards[rt.rank]).tobytes()
         assert got == leaf[2].tobytes(), path
+    from paper_2605_23066_b200 import timeline
+
+    assert "ipc_publish" in timeline.LAST_RESTORE[rt.rank]  # replicas: ranks write to each other
+    # same sharding as saved: every chunk lands in its reader's own process -> no IPC at all
+    mesh1 = tv.Mesh.create([("fsdp", world)], process_count=world)
+    out = tv.load_checkpoint(rt, "ck/run_0", None, current_mesh=mesh1)
+    assert "ipc_publish" not in timeline.LAST_RESTORE[rt.rank], timeline.LAST_RESTORE[rt.rank]
+    for path, leaf in leaves.items():
+        if path.startswith("extra/"):
+            continue
+        node = out["state"]
+        for p in path.split("/"):
+            node = node[p]
+        ranges = dict((sh.device, sh.ranges) for sh in tv.shards_of(shardings[path]))[rt.rank]
+        sel = tuple(slice(o, o + e) for o, e in ranges)
+        got = tv.DenseArray(leaf[1], node.shards[rt.rank]).tobytes()
+        assert got == np.ascontiguousarray(leaf[2][sel]).tobytes(), path
+    # fused cast across processes: f32 leaves restored as f64 onto the replica mesh (the
+    # reader's kernel converts while storing into the peer's arena)
+    cast_abs = {}
+    for path, leaf in leaves.items():
+        if leaf[1] != "f32":
+            continue
+        node = cast_abs
+        parts = path.split("/")
+        for p in parts[:-1]:
+            node = node.setdefault(p, {})
+        node[parts[-1]] = tv.AbstractLeaf("array", leaf[2].shape, "f64", tv.Sharding(
+            mesh2, tv.PartitionSpec(("fsdp",) + (None,) * (leaf[2].ndim - 1)), leaf[2].shape))
+    out = tv.load_checkpoint(rt, "ck/run_1", {"state": cast_abs}, tv.LoadOptions(mode="partial"))
+    n_cast = 0
+    for path, leaf in leaves.items():
+        if leaf[1] != "f32":
+            continue
+        node = out["state"]
+        for p in path.split("/"):
+            node = node[p]
+        got = tv.DenseArray("f64", node.shards[rt.rank]).tobytes()
+        assert got == leaf[2].astype(np.float64).tobytes(), path
+        n_cast += 1
+    assert n_cast > 0
     rt.local.barrier("done")
     dist.destroy_process_group()
 
