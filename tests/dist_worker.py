@@ -11,6 +11,7 @@ Exit code 0 = pass.
 
 from __future__ import annotations
 
+import datetime
 import os
 import sys
 
@@ -26,9 +27,9 @@ def coord(base: str) -> None:
     import paper_2605_23066_b200 as tv
     from paper_2605_23066_b200 import save_pipeline
 
-    dist.init_process_group("gloo")
+    dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=90))  # fail, never hang
     backend = tv.FilesystemBackend(base)
-    rt = tv.DistributedRuntime(backend)
+    rt = tv.DistributedRuntime(backend, barrier_timeout=90.0)
     rank, world = rt.rank, rt.process_count
     ctx = rt.local
     ctx.barrier("a")
@@ -67,9 +68,9 @@ def datapath(base: str) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     gpu = local % torch.cuda.device_count()
     torch.cuda.set_device(gpu)
-    dist.init_process_group("gloo")
+    dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=90))  # fail, never hang
     backend = tv.FilesystemBackend(base)
-    rt = tv.DistributedRuntime(backend, gpu=gpu)
+    rt = tv.DistributedRuntime(backend, gpu=gpu, barrier_timeout=90.0)
     world = rt.process_count
     rng = np.random.default_rng(3)
     tree = {"state": cases.llama_like(rng, layers=1, d=32, ffn=48, vocab=40, kv=8)}
@@ -134,9 +135,18 @@ def datapath(base: str) -> None:
     from paper_2605_23066_b200 import timeline
 
     assert "ipc_publish" in timeline.LAST_RESTORE[rt.rank]  # replicas: ranks write to each other
-    # same sharding as saved: every chunk lands in its reader's own process -> no IPC at all
-    mesh1 = tv.Mesh.create([("fsdp", world)], process_count=world)
-    out = tv.load_checkpoint(rt, "ck/run_0", None, current_mesh=mesh1)
+    # same sharding as saved (sharded leaves only: the unsharded one fans out from process
+    # 0): every chunk lands in its reader's own process -> no IPC at all
+    same_abs = {}
+    for path, leaf in leaves.items():
+        if path.startswith("extra/"):
+            continue
+        node = same_abs
+        parts = path.split("/")
+        for p in parts[:-1]:
+            node = node.setdefault(p, {})
+        node[parts[-1]] = tv.AbstractLeaf("array", leaf[2].shape, leaf[1], shardings[path])
+    out = tv.load_checkpoint(rt, "ck/run_0", {"state": same_abs}, tv.LoadOptions(mode="partial"))
     assert "ipc_publish" not in timeline.LAST_RESTORE[rt.rank], timeline.LAST_RESTORE[rt.rank]
     for path, leaf in leaves.items():
         if path.startswith("extra/"):
