@@ -52,6 +52,20 @@ def coord(base: str) -> None:
     assert pieces == [(((8 * rank, 8), (0, 4)), rank)], pieces
     gathered = rt.all_gather_object(pieces)
     assert len(gathered) == world
+    # one Checkpointer per rank: retention deletes happen once (process 0), every rank's
+    # catalog agrees, no rank sees another's deletion as a failure
+    for background in (False, True):
+        root = f"loop_{int(background)}"
+        ck = tv.Checkpointer(rt, root, tv.RetentionPolicy(keep_last=2), tv.SaveOptions(sync=False),
+                             background_delete=background)
+        for step in range(5):
+            ck.save_step(step, {"m": {"step": tv.Scalar("i64", step)}})
+        ck.close()
+        assert ck.all_steps() == [3, 4], ck.all_steps()
+        ctx.barrier(f"loop{background}")
+        assert sorted(tv.Checkpointer(rt, root).all_steps()) == [3, 4]
+        got = ck.load_step()
+        assert got["m"]["step"] == tv.Scalar("i64", 4)
     ctx.barrier("done")
     dist.destroy_process_group()
 
