@@ -656,6 +656,7 @@ def run_c5(args) -> dict:
     ck = tv.Checkpointer(rt, "run", tv.RetentionPolicy(keep_last=3), tv.SaveOptions(sync=False),
                          background_delete=not args.inline_gc)
     blocking, waits, joins, gcs, bg = [], [], [], [], []
+    phase_sums: dict[str, float] = {}
     t_start = time.perf_counter()
     for step in range(args.steps):
         # synthetic training step: fixed GPU time + an in-place update of every param shard
@@ -670,7 +671,11 @@ def run_c5(args) -> dict:
         waits.append(d.max(ck.last_wait_seconds * 1e3))
         joins.append(d.max(ck.last_join_seconds * 1e3))
         gcs.append(d.max(ck.last_gc_seconds * 1e3))
-        if step > 0:
+        if step > 0:  # the previous save has been joined: its per-phase timeline is final
+            from paper_2605_23066_b200 import timeline as _tlm
+
+            for k, v in _tlm.LAST_SAVE.get(d.rank if d.on else 0, {}).items():
+                phase_sums[k] = phase_sums.get(k, 0.0) + v
             tl = prev.handles[0].session.timeline
             if "finalized" in tl and "snapshotted" in tl:
                 bg.append((tl["finalized"] - tl["snapshotted"]) * 1e3)
@@ -707,6 +712,7 @@ def run_c5(args) -> dict:
         "blocking_frac_of_sync_save": round(statistics.mean(steady) / sync_save_ms, 4),
         "loop_seconds": round(loop_s, 2),
         "retained_steps": kept,
+        "save_phases_ms_mean_rank0": {k: round(v / max(1, args.steps - 1), 2) for k, v in phase_sums.items()},
     }
     d.barrier()
     if d.rank == 0:
