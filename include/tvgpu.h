@@ -189,6 +189,13 @@ int tv_ipc_export(int device, uint64_t ptr, uint8_t handle_out[64], uint64_t* ba
 int tv_ipc_import(int device, const uint8_t handle[64], uint64_t* ptr_out);
 int tv_ipc_close(int device, uint64_t ptr);
 
+/* ---- bulk delete ------------------------------------------------------------------- */
+/* Unlink n files on n_threads native threads (retention deletes of a whole checkpoint:
+ * freeing tmpfs pages is per-inode kernel work; native threads keep it off the caller's
+ * interpreter lock).  ok[i] = 1 if paths[i] was removed, 0 if it did not exist; any other
+ * failure returns TV_ERR_IO with the first failing path (training_manager.py:262-279). */
+int tv_unlink_many(const char* const* paths, int n, int n_threads, uint8_t* ok);
+
 /* ---- roofline probes (same run as the numbers they bound) ------------------------- */
 /* fio-style sequential write then read of n_threads files of file_bytes each, in
  * block_bytes pwrite/pread calls from pinned memory.  Files are removed afterwards. */

@@ -108,6 +108,39 @@ int tv_engine_load(tv_engine* e, const tv_read_item* items, int n_items, const t
   return tv::engine_load(e, items, n_items, inputs, n_inputs, copies, n_copies, stats);
 }
 
+int tv_unlink_many(const char* const* paths, int n, int n_threads, uint8_t* ok) {
+  if (n < 0 || (n > 0 && (!paths || !ok))) {
+    tv::set_error("tv_unlink_many: bad arguments");
+    return TV_ERR_ARG;
+  }
+  const int t = std::max(1, std::min(n_threads, std::max(1, n)));
+  std::atomic<int> next{0};
+  std::atomic<int> failed{-1};
+  std::atomic<int> err_no{0};
+  auto work = [&] {
+    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) {
+      if (::unlink(paths[i]) == 0) {
+        ok[i] = 1;
+      } else {
+        ok[i] = 0;
+        if (errno != ENOENT && errno != ENOTDIR) {
+          int expect = -1;
+          if (failed.compare_exchange_strong(expect, i)) err_no.store(errno);
+        }
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < t; ++k) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  if (failed.load() >= 0) {
+    tv::set_error(std::string("unlink ") + paths[failed.load()] + ": " + std::strerror(err_no.load()));
+    return TV_ERR_IO;
+  }
+  return TV_OK;
+}
+
 int tv_enable_peer_access(const int* devices, int n) {
   tv::DeviceGuard guard;
   for (int i = 0; i < n; ++i) {

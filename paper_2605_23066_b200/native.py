@@ -67,6 +67,7 @@ EXPORTS = (
     "tv_kernel_timing_collect", "tv_engine_create",
     "tv_engine_destroy", "tv_engine_save", "tv_engine_load", "tv_enable_peer_access",
     "tv_ipc_export", "tv_ipc_import", "tv_ipc_close", "tv_probe_storage", "tv_probe_pcie",
+    "tv_unlink_many",
 )
 
 _lib = None
@@ -93,6 +94,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tv_ipc_close": (I, [I, ctypes.c_uint64]),
         "tv_probe_storage": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "tv_probe_pcie": (I, [I, L, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
+        "tv_unlink_many": (I, [P, I, I, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -282,6 +284,21 @@ def ipc_import(device: int, handle: bytes) -> int:
 
 def ipc_close(device: int, ptr: int) -> None:
     check(lib().tv_ipc_close(device, ptr), "tv_ipc_close")
+
+
+def unlink_many(paths: Sequence[str], threads: int) -> list[bool]:
+    """Remove files on native threads (no interpreter lock held); True = removed, False =
+    did not exist.  Raises BackendError on any other failure."""
+    if not paths:
+        return []
+    table = PathTable(list(paths))
+    ok = np.zeros(len(paths), np.uint8)
+    rc = lib().tv_unlink_many(table.pointers.ctypes.data, len(paths), int(threads), ok.ctypes.data)
+    if rc != 0:
+        from .errors import BackendError
+
+        raise BackendError(last_error())
+    return [bool(x) for x in ok]
 
 
 def probe_storage(directory: str, threads: int, file_bytes: int, block_bytes: int) -> tuple[float, float]:

@@ -88,3 +88,19 @@ def test_engine_sizing_rules(monkeypatch):
     assert native.EngineConfig().sizing(1) == native.EngineConfig().sizing(4)
     monkeypatch.setenv("TVGPU_SLOT_BYTES", str(1 << 20))
     assert native.EngineConfig().sizing(1)[1] == 1 << 20
+
+
+def test_unlink_many(tmp_path):
+    """Native bulk unlink (no GPU needed): removed / absent flags; other errors raise."""
+    from paper_2605_23066_b200 import native
+    from paper_2605_23066_b200.errors import BackendError
+
+    files = [tmp_path / f"f{i}" for i in range(50)]
+    for f in files:
+        f.write_bytes(b"x" * 100)
+    got = native.unlink_many([str(f) for f in files] + [str(tmp_path / "missing")], 8)
+    assert got == [True] * 50 + [False]
+    assert not any(f.exists() for f in files)
+    (tmp_path / "d").mkdir()
+    with pytest.raises(BackendError):
+        native.unlink_many([str(tmp_path / "d")], 2)
