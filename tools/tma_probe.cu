@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #define CK(x)                                                                     \
   do {                                                                            \
@@ -27,8 +28,7 @@
     }                                                                             \
   } while (0)
 
-constexpr int kBlock = 32 * 1024;  // bytes per TMA transfer
-constexpr int kStages = 6;         // 192 KiB of shared memory per CTA
+constexpr int kBlock = 16 * 1024;  // granularity of the copied size (lcm of variants' blocks)
 
 __global__ void __launch_bounds__(256) ldst_copy(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                  int64_t n_vec) {
@@ -55,6 +55,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+template <int kStages, int kBlock>
 __global__ void __launch_bounds__(32) tma_copy(const char* __restrict__ src, char* __restrict__ dst,
                                                int64_t n_blocks) {
   extern __shared__ __align__(128) char smem[];
@@ -107,6 +108,60 @@ __global__ void __launch_bounds__(32) tma_copy(const char* __restrict__ src, cha
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+
+// Same ring, but a stage is refilled one iteration after its store was issued, so one
+// bulk store stays in flight while the next load is issued (wait_group.read 1).
+template <int kStages, int kBlock>
+__global__ void __launch_bounds__(32) tma_copy2(const char* __restrict__ src, char* __restrict__ dst,
+                                                int64_t n_blocks) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t full[kStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint32_t phase[kStages] = {0};
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  int64_t issued = first;
+  for (int s = 0; s < kStages && issued < n_blocks; ++s, issued += step) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                 "r"(kBlock));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem + s * kBlock)),
+        "l"(src + issued * kBlock), "r"(kBlock), "r"(smem_u32(&full[s]))
+        : "memory");
+  }
+  int s = 0, prev = -1;
+  for (int64_t b = first; b < n_blocks; b += step) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(&full[s])),
+        "r"(phase[s])
+        : "memory");
+    phase[s] ^= 1;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + b * kBlock),
+                 "r"(smem_u32(smem + s * kBlock)), "r"(kBlock)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (prev >= 0 && issued < n_blocks) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // prev stage's store read
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[prev])),
+                   "r"(kBlock));
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(smem + prev * kBlock)),
+          "l"(src + issued * kBlock), "r"(kBlock), "r"(smem_u32(&full[prev]))
+          : "memory");
+      issued += step;
+    }
+    prev = s;
+    s = (s + 1) % kStages;
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main(int argc, char** argv) {
   const double gib = argc > 1 ? std::atof(argv[1]) : 8.0;
   int64_t bytes = (int64_t)(gib * (1 << 30));
@@ -117,8 +172,6 @@ int main(int argc, char** argv) {
   CK(cudaMemset(a, 1, bytes));
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int smem = kStages * kBlock;
-  CK(cudaFuncSetAttribute(tma_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -144,19 +197,50 @@ int main(int argc, char** argv) {
   time_it("ldst_grid_full", [&] {
     ldst_copy<<<(unsigned)((n_vec + 2047) / 2048), 256>>>((const uint4*)a, (uint4*)b, n_vec);
   });
-  for (int per_sm : {1}) {
-    char name[64];
-    std::snprintf(name, sizeof name, "tma_%dx%d_stages%d_%dKiB", sms, per_sm, kStages, kBlock / 1024);
-    time_it(name, [&] { tma_copy<<<sms * per_sm, 32, smem>>>(a, b, bytes / kBlock); });
-  }
+  auto tma = [&](auto stages_c, auto block_c, int per_sm) {
+    constexpr int S = decltype(stages_c)::value, B = decltype(block_c)::value;
+    const int smem = S * B;
+    CK(cudaFuncSetAttribute(tma_copy<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    char name[96];
+    std::snprintf(name, sizeof name, "tma_%dx%d_stages%d_%dKiB", sms, per_sm, S, B / 1024);
+    time_it(name, [&] { tma_copy<S, B><<<sms * per_sm, 32, smem>>>(a, b, bytes / B); });
+  };
+  auto tma2 = [&](auto stages_c, auto block_c, int per_sm) {
+    constexpr int S = decltype(stages_c)::value, B = decltype(block_c)::value;
+    const int smem = S * B;
+    CK(cudaFuncSetAttribute(tma_copy2<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    char name[96];
+    std::snprintf(name, sizeof name, "tma2_%dx%d_stages%d_%dKiB", sms, per_sm, S, B / 1024);
+    time_it(name, [&] { tma_copy2<S, B><<<sms * per_sm, 32, smem>>>(a, b, bytes / B); });
+  };
+  using std::integral_constant;
+  tma2(integral_constant<int, 6>{}, integral_constant<int, 32768>{}, 1);
+  tma2(integral_constant<int, 12>{}, integral_constant<int, 16384>{}, 1);
+  tma2(integral_constant<int, 6>{}, integral_constant<int, 16384>{}, 2);
+  tma2(integral_constant<int, 3>{}, integral_constant<int, 65536>{}, 1);
+  tma(integral_constant<int, 6>{}, integral_constant<int, 32768>{}, 1);
+  tma(integral_constant<int, 3>{}, integral_constant<int, 32768>{}, 2);
+  tma(integral_constant<int, 6>{}, integral_constant<int, 16384>{}, 2);
+  tma(integral_constant<int, 3>{}, integral_constant<int, 65536>{}, 1);
+  tma(integral_constant<int, 4>{}, integral_constant<int, 16384>{}, 3);
+  tma(integral_constant<int, 12>{}, integral_constant<int, 16384>{}, 1);
   time_it("ce_memcpy_d2d", [&] { CK(cudaMemcpyAsync(b, a, bytes, cudaMemcpyDeviceToDevice)); });
   // correctness of the TMA path
   CK(cudaMemset(b, 0, bytes));
   CK(cudaMemset(a, 0x5a, bytes));
-  tma_copy<<<sms, 32, smem>>>(a, b, bytes / kBlock);
+  tma_copy<6, 32768><<<sms, 32, 6 * 32768>>>(a, b, bytes / 32768);
   CK(cudaDeviceSynchronize());
   unsigned char probe[4] = {0};
   CK(cudaMemcpy(probe, b + bytes - 4, 4, cudaMemcpyDeviceToHost));
   std::printf("{\"tma_tail_ok\": %s}\n", probe[0] == 0x5a && probe[3] == 0x5a ? "true" : "false");
+  CK(cudaMemset(b, 0, bytes));
+  CK(cudaFuncSetAttribute(tma_copy2<6, 32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768));
+  tma_copy2<6, 32768><<<sms, 32, 6 * 32768>>>(a, b, bytes / 32768);
+  CK(cudaDeviceSynchronize());
+  unsigned char* hb = (unsigned char*)std::malloc(bytes);
+  CK(cudaMemcpy(hb, b, bytes, cudaMemcpyDeviceToHost));
+  int64_t bad = 0;
+  for (int64_t i = 0; i < bytes; ++i) bad += hb[i] != 0x5a;
+  std::printf("{\"tma2_all_bytes_ok\": %s}\n", bad == 0 ? "true" : "false");
   return 0;
 }
