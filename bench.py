@@ -276,19 +276,20 @@ def make_workload(tv, args, N) -> Workload:
     if cfg == "c1":
         leaves = [("model", f"a{i}", (4096, 4096), "f32") for i in range(4)]
         mesh = tv.Mesh.create([("solo", 1)], process_count=1)
-        return Workload(tv, "c1", leaves, mesh, lambda s: None, tv.SaveOptions(sync=True),
+        return Workload(tv, "c1", leaves, mesh, lambda s: None, tv.SaveOptions(sync=True, layout=args.layout),
                         describe="C1 4 x (4096,4096) f32 unsharded, process 0 writes, " + args.save_mode + " save -> restore")
     if cfg == "c2":
         mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
-        return Workload(tv, "c2", llama, mesh, fsdp_spec, tv.SaveOptions(sync=True),
+        return Workload(tv, "c2", llama, mesh, fsdp_spec, tv.SaveOptions(sync=True, layout=args.layout),
                         describe=f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu, FSDP-{N} on dim 0, "
-                                 f"{args.save_mode} save -> restore, per_leaf layout")
+                                 f"{args.save_mode} save -> restore, {args.layout} layout")
     if cfg in ("c3", "c3ss"):
         if N % 2:
             raise SystemExit("c3 needs an even number of GPUs (replica 2 x fsdp N/2)")
         mesh = tv.Mesh.create([("replica", 2), ("fsdp", N // 2)], process_count=N, replica_axis="replica")
         rp = cfg == "c3"
-        return Workload(tv, cfg, llama, mesh, fsdp_spec, tv.SaveOptions(sync=True, replica_parallel=rp),
+        return Workload(tv, cfg, llama, mesh, fsdp_spec,
+                        tv.SaveOptions(sync=True, replica_parallel=rp, layout=args.layout),
                         describe=f"C3 Llama-3-8B on a 2x{N // 2} (replica x fsdp) mesh, "
                                  f"{'replica-parallel' if rp else 'single-slice'} {args.save_mode} save -> restore")
     if cfg == "c4":
@@ -297,7 +298,8 @@ def make_workload(tv, args, N) -> Workload:
         Pr = args.restore_gpus or N
         save_mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
         rmesh = tv.Mesh.create([("replica", 2), ("fsdp", Pr // 2)], process_count=Pr, replica_axis="replica")
-        return Workload(tv, "c4", llama, save_mesh, fsdp_spec, tv.SaveOptions(sync=True), restore_mesh=rmesh,
+        return Workload(tv, "c4", llama, save_mesh, fsdp_spec, tv.SaveOptions(sync=True, layout=args.layout),
+                        restore_mesh=rmesh,
                         restore_P=Pr,
                         describe=f"C4 Llama-3-8B saved 1x{N} (FSDP-{N}) -> restored onto 2x{Pr // 2} "
                                  f"(replica x fsdp, {Pr} GPUs), read-once + NVLink fan-out")
@@ -1090,6 +1092,8 @@ def main() -> None:
                     help="hugetmpfs (default; falls back to /dev/shm if it cannot be mounted) or shm")
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c3ss", "c4", "c5"])
     ap.add_argument("--restore-gpus", type=int, default=None)
+    ap.add_argument("--layout", default="per_leaf", choices=["per_leaf", "aggregated"],
+                    help="per_leaf (one file per chunk, default) or aggregated (64 MiB data files + manifest)")
     ap.add_argument("--save-mode", default="async", choices=["async", "sync"],
                     help="async (default): each step's save is an async save + wait; sync: sync save")
     ap.add_argument("--no-e2e", action="store_true")
