@@ -452,9 +452,18 @@ def run_ours(args) -> dict:
         probe["storage_write_GBps"], probe["storage_read_GBps"] = round(best[0], 2), round(best[1], 2)
         probe["storage_threads"] = nthreads
         probe["storage_probe"] = f"{nthreads} threads x 1 GiB files, 8 MiB pwrite/pread from pinned memory, best of 2"
+    d.barrier()  # every rank probes its own link at the same time: the aggregate is concurrent
     d2h, h2d = native.probe_pcie(d.local if d.on else 0, 1 << 30, 3)
     probe["pcie_d2h_GBps_per_gpu"] = round(d2h, 2)
     probe["pcie_h2d_GBps_per_gpu"] = round(h2d, 2)
+    if d.on:
+        probe["pcie_d2h_GBps_aggregate"] = round(d.sum(d2h), 2)
+        probe["pcie_h2d_GBps_aggregate"] = round(d.sum(h2d), 2)
+        probe["pcie_aggregate_how"] = "all ranks' pinned 1 GiB D2H / H2D measured concurrently, summed"
+    else:
+        probe["pcie_d2h_GBps_aggregate"] = round(d2h * N, 2)
+        probe["pcie_h2d_GBps_aggregate"] = round(h2d * N, 2)
+        probe["pcie_aggregate_how"] = "GPU 0's link x GPUs" if N > 1 else "one GPU"
     d.barrier()
 
     clocks = ClockSampler()
@@ -600,8 +609,8 @@ def run_ours(args) -> dict:
         },
     }
     if d.rank == 0:
-        pcie_d2h = probe["pcie_d2h_GBps_per_gpu"] * N
-        pcie_h2d = probe["pcie_h2d_GBps_per_gpu"] * N
+        pcie_d2h = probe["pcie_d2h_GBps_aggregate"]
+        pcie_h2d = probe["pcie_h2d_GBps_aggregate"]
         save_peak = min(probe["storage_write_GBps"], pcie_d2h)
         restore_peak = min(probe["storage_read_GBps"], pcie_h2d)
         result["io_roofline"] = {
