@@ -429,7 +429,7 @@ class EngineConfig:
         if self.threads:
             return self.threads
         engines = self._engines(concurrent)
-        return max(2, (_host_cores() - engines) // engines)
+        return max(2, min(64, (_host_cores() - engines) // engines))  # measured up to 28; cap huge hosts
 
     def sizing(self, concurrent: int) -> tuple[int, int, int, int]:
         """(n_slots, slot_bytes, staging_bytes, threads) for an engine of this box."""
