@@ -559,7 +559,8 @@ def run_ours(args) -> dict:
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "bf16+f32 bytes (pure data movement)",
+        "dtype": "u8",
+        "payload_dtypes": "bf16 params + f32 Adam mu/nu, moved as bytes (no arithmetic on the path)",
         "data": "synthetic (random values generated on device, Llama-3-8B shapes)",
         "config": {
             "workload": wl.describe + f", {len(wl.leaves)} leaves, {tree_bytes} bytes",
@@ -1074,7 +1075,8 @@ def run_reference(args) -> dict:
         "steps": args.steps,
         "warmup": args.warmup,
         "higher_is_better": True,
-        "dtype": "bf16+f32 bytes (pure data movement)",
+        "dtype": "u8",
+        "payload_dtypes": "bf16 params + f32 Adam mu/nu, moved as bytes (no arithmetic on the path)",
         "data": "synthetic (numpy RNG, Llama-3-8B shapes)",
         "config": {"workload": f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu (bounded sample: {res['sample']})",
                    "config": "c2", "storage": f"oracle port writing/reading {args.dir} (tmpfs)"},
