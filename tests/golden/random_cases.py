@@ -12,7 +12,7 @@ import numpy as np
 
 import cases
 
-N_CASES = 40
+N_CASES = 120
 
 MESHES = [
     ([("fsdp", 2)], None), ([("fsdp", 4)], None), ([("fsdp", 8)], None),

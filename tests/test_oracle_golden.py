@@ -90,7 +90,7 @@ def test_oracle_shard_bytes_match_reference_digests():
 
 
 def test_oracle_reproduces_reference_on_random_cases():
-    """The oracle's stored bytes equal the real reference's on 40 random save cases
+    """The oracle's stored bytes equal the real reference's on 120 random save cases
     (random meshes / specs / dtypes / layouts / replica-parallel / subchunking)."""
     import hashlib
 
