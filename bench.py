@@ -129,11 +129,18 @@ def measured_peaks() -> dict:
 
 
 class Dist:
+    """torchrun plumbing of the bench: NCCL process group, one rank per GPU.  When there
+    are more local ranks than GPUs (a robustness run of the 8-rank path on a smaller box)
+    ranks share GPUs round-robin and the bench's own collectives go over gloo (NCCL
+    refuses two ranks on one GPU)."""
+
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
-        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.local = self.local_rank
         self.on = self.world > 1
+        self.dev = "cuda"
 
     def init(self):
         import datetime
@@ -141,10 +148,17 @@ class Dist:
         import torch
         import torch.distributed as dist
 
+        n = max(1, torch.cuda.device_count())
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(self.world)))
+        self.local = self.local_rank % n
         if self.on and not dist.is_initialized():
             torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local),
-                                    timeout=datetime.timedelta(seconds=1800))
+            if local_world > n:
+                self.dev = "cpu"
+                dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=1800))
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local),
+                                        timeout=datetime.timedelta(seconds=1800))
 
     def barrier(self):
         if self.on:
@@ -153,25 +167,27 @@ class Dist:
             if dist.is_initialized():
                 dist.barrier()
 
-    def max(self, x: float) -> float:
-        if not self.on:
-            return x
+    def _reduce(self, x: float, op) -> float:
         import torch
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(t, op=op)
         return float(t.item())
+
+    def max(self, x: float) -> float:
+        if not self.on:
+            return x
+        import torch.distributed as dist
+
+        return self._reduce(x, dist.ReduceOp.MAX)
 
     def sum(self, x: float) -> float:
         if not self.on:
             return x
-        import torch
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return self._reduce(x, dist.ReduceOp.SUM)
 
 
 # -- workload ------------------------------------------------------------------------------------
