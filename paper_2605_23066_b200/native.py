@@ -403,7 +403,7 @@ class EngineConfig:
 
     threads  — host cores shared by the engines running at once on this box (the
                threads runtime's processes, or torchrun's LOCAL_WORLD_SIZE ranks), minus
-               one core per engine for its producer;
+               one core per engine for its producer when an engine has >= 8 cores;
     n_slots  — 2 pinned slots per storage thread (fewer starves the readers);
     slot     — 4 MiB for a single engine (fewer, larger DMAs); with several engines
                2 MiB, or 1 MiB when the rings of all engines would not fit the host's
@@ -429,7 +429,10 @@ class EngineConfig:
         if self.threads:
             return self.threads
         engines = self._engines(concurrent)
-        return max(2, min(64, (_host_cores() - engines) // engines))  # measured up to 28; cap huge hosts
+        per = _host_cores() // engines
+        # a core for the producer only when there are >= 8 per engine (measured: 15 of 16
+        # and 7 of 8 beat all cores; 4 of 4 beats 3 — profiles/r01_ab_threads_*.txt)
+        return max(2, min(64, per - 1 if per >= 8 else per))
 
     def sizing(self, concurrent: int) -> tuple[int, int, int, int]:
         """(n_slots, slot_bytes, staging_bytes, threads) for an engine of this box."""

@@ -71,9 +71,10 @@ def test_no_gpu_means_loud_failure():
 
 
 def test_engine_sizing_rules(monkeypatch):
-    """Measured sizing (profiles/r01_ab_slot_*.txt, r01_ab_threads_per_engine.txt): one
-    engine owning the host gets 4 MiB slots and cores - 1 storage threads; engines sharing
-    the host split the cores and use <= 2 MiB slots; 2 slots per thread (>= 16)."""
+    """Measured sizing (profiles/r01_ab_slot_*.txt, r01_ab_threads_*.txt): one engine
+    owning the host gets 4 MiB slots and cores - 1 storage threads; engines sharing the host
+    split the cores (one kept for the producer only at >= 8 each) and use <= 2 MiB slots;
+    2 slots per thread (>= 16)."""
     from paper_2605_23066_b200 import native
 
     monkeypatch.delenv("LOCAL_WORLD_SIZE", raising=False)
@@ -83,7 +84,10 @@ def test_engine_sizing_rules(monkeypatch):
     n_slots, slot, staging, threads = native.EngineConfig().sizing(1)
     assert (slot, threads, n_slots) == (4 << 20, 15, 30) and staging >= n_slots * slot
     n_slots, slot, staging, threads = native.EngineConfig().sizing(4)
-    assert threads == 3 and slot <= 2 << 20 and n_slots == 16
+    assert threads == 4 and slot <= 2 << 20 and n_slots == 16  # 4 cores each: no producer core
+    monkeypatch.setattr(native, "_host_cores", lambda: 32)
+    assert native.EngineConfig().sizing(4)[3] == 7                 # 8 cores each: one for the producer
+    monkeypatch.setattr(native, "_host_cores", lambda: 16)
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "4")
     assert native.EngineConfig().sizing(1) == native.EngineConfig().sizing(4)
     monkeypatch.setenv("TVGPU_SLOT_BYTES", str(1 << 20))
