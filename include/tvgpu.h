@@ -201,6 +201,12 @@ int tv_unlink_many(const char* const* paths, int n, int n_threads, uint8_t* ok);
  * block_bytes pwrite/pread calls from pinned memory.  Files are removed afterwards. */
 int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
                      double* write_gbps, double* read_gbps);
+/* The same storage probe while a DMA thread keeps `device`'s copy engine busy for the
+ * whole window (D2H during the writes, H2D during the reads): the contended rates of a
+ * copy-through-pinned pipeline, whose DMA and page-cache copies share host memory. */
+int tv_probe_storage_dma(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
+                         int device, double* write_gbps, double* read_gbps, double* d2h_gbps,
+                         double* h2d_gbps);
 /* Pinned D2H and H2D copy bandwidth of `device` over `bytes` (best of `reps`). */
 int tv_probe_pcie(int device, int64_t bytes, int reps, double* d2h_gbps, double* h2d_gbps);
 

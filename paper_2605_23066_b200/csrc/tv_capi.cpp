@@ -216,8 +216,15 @@ static double wall() {
       .count();
 }
 
-int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
-                     double* write_gbps, double* read_gbps) {
+namespace {
+
+// fio-style probe: n_threads files of file_bytes, block_bytes pwrite then pread from
+// pinned memory.  With device >= 0 a DMA thread keeps that GPU's copy engine busy for
+// the whole window (D2H during the writes, H2D during the reads) and its rate is
+// returned too: the contended rates of a copy-through-pinned pipeline.
+int probe_storage_impl(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
+                       int device, double* write_gbps, double* read_gbps, double* d2h_gbps,
+                       double* h2d_gbps) {
   if (!dir || n_threads < 1 || file_bytes < 1 || block_bytes < 1) {
     tv::set_error("tv_probe_storage: bad arguments");
     return TV_ERR_ARG;
@@ -233,9 +240,37 @@ int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t
     }
     std::memset(b, 0x5a, block_bytes);
   }
+  const int64_t dma_bytes = 64ll << 20;
+  char *dbuf = nullptr, *hbuf = nullptr;
+  cudaStream_t st = nullptr;
+  if (device >= 0) {
+    cudaSetDevice(device);
+    if (cudaMalloc(&dbuf, dma_bytes) != cudaSuccess || cudaHostAlloc(&hbuf, dma_bytes, cudaHostAllocDefault) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+      tv::set_error("probe: DMA buffers");
+      return TV_ERR_NOMEM;
+    }
+  }
   auto path = [&](int t) { return std::string(dir) + "/.tvgpu_probe_" + std::to_string(t); };
   std::atomic<int> failed{0};
-  auto run = [&](bool write) {
+  auto run = [&](bool write, double* dma_gbps) {
+    std::atomic<bool> stop{false};
+    std::atomic<int64_t> moved{0};
+    double d0 = 0, d1 = 0;
+    std::thread dma;
+    if (device >= 0) {
+      dma = std::thread([&] {
+        cudaSetDevice(device);
+        d0 = wall();
+        while (!stop.load()) {
+          if (write) cudaMemcpyAsync(hbuf, dbuf, dma_bytes, cudaMemcpyDeviceToHost, st);
+          else cudaMemcpyAsync(dbuf, hbuf, dma_bytes, cudaMemcpyHostToDevice, st);
+          cudaStreamSynchronize(st);
+          moved += dma_bytes;
+        }
+        d1 = wall();
+      });
+    }
     std::vector<std::thread> th;
     double t0 = wall();
     for (int t = 0; t < n_threads; ++t)
@@ -262,17 +297,48 @@ int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t
         ::close(fd);
       });
     for (auto& x : th) x.join();
-    return (double)file_bytes * n_threads / (wall() - t0) / 1e9;
+    const double gbps = (double)file_bytes * n_threads / (wall() - t0) / 1e9;
+    if (device >= 0) {
+      stop = true;
+      dma.join();
+      if (dma_gbps) *dma_gbps = (double)moved.load() / std::max(1e-9, d1 - d0) / 1e9;
+    }
+    return gbps;
   };
-  *write_gbps = run(true);
-  *read_gbps = run(false);
+  *write_gbps = run(true, d2h_gbps);
+  *read_gbps = run(false, h2d_gbps);
   for (int t = 0; t < n_threads; ++t) ::unlink(path(t).c_str());
   for (auto b : bufs) cudaFreeHost(b);
+  if (device >= 0) {
+    cudaStreamDestroy(st);
+    cudaFree(dbuf);
+    cudaFreeHost(hbuf);
+  }
   if (failed) {
     tv::set_error(std::string("probe I/O failed in ") + dir);
     return TV_ERR_IO;
   }
   return TV_OK;
+}
+
+}  // namespace
+
+int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
+                     double* write_gbps, double* read_gbps) {
+  return probe_storage_impl(dir, n_threads, file_bytes, block_bytes, -1, write_gbps, read_gbps,
+                            nullptr, nullptr);
+}
+
+int tv_probe_storage_dma(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
+                         int device, double* write_gbps, double* read_gbps, double* d2h_gbps,
+                         double* h2d_gbps) {
+  tv::DeviceGuard guard;
+  if (device < 0) {
+    tv::set_error("tv_probe_storage_dma: needs a device");
+    return TV_ERR_ARG;
+  }
+  return probe_storage_impl(dir, n_threads, file_bytes, block_bytes, device, write_gbps, read_gbps,
+                            d2h_gbps, h2d_gbps);
 }
 
 int tv_probe_pcie(int device, int64_t bytes, int reps, double* d2h_gbps, double* h2d_gbps) {

@@ -67,7 +67,7 @@ EXPORTS = (
     "tv_kernel_timing_collect", "tv_engine_create",
     "tv_engine_destroy", "tv_engine_save", "tv_engine_load", "tv_enable_peer_access",
     "tv_ipc_export", "tv_ipc_import", "tv_ipc_close", "tv_probe_storage", "tv_probe_pcie",
-    "tv_unlink_many",
+    "tv_unlink_many", "tv_probe_storage_dma",
 )
 
 _lib = None
@@ -95,6 +95,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tv_probe_storage": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "tv_probe_pcie": (I, [I, L, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "tv_unlink_many": (I, [P, I, I, P]),
+        "tv_probe_storage_dma": (I, [ctypes.c_char_p, I, L, L, I, ctypes.POINTER(D), ctypes.POINTER(D),
+                                     ctypes.POINTER(D), ctypes.POINTER(D)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -309,6 +311,17 @@ def probe_storage(directory: str, threads: int, file_bytes: int, block_bytes: in
         "tv_probe_storage",
     )
     return w.value, r.value
+
+
+def probe_storage_dma(directory: str, threads: int, file_bytes: int, block_bytes: int,
+                      device: int) -> tuple[float, float, float, float]:
+    """(write, read, D2H, H2D) GB/s with the storage probe and a DMA loop running at once."""
+    os.makedirs(directory, exist_ok=True)
+    w, r, d2h, h2d = (ctypes.c_double() for _ in range(4))
+    check(lib().tv_probe_storage_dma(directory.encode(), threads, file_bytes, block_bytes, device,
+                                     ctypes.byref(w), ctypes.byref(r), ctypes.byref(d2h),
+                                     ctypes.byref(h2d)), "tv_probe_storage_dma")
+    return w.value, r.value, d2h.value, h2d.value
 
 
 def probe_pcie(device: int, nbytes: int = 1 << 30, reps: int = 3) -> tuple[float, float]:
