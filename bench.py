@@ -484,7 +484,8 @@ def run_ours(args) -> dict:
     # writes, H2D during the reads): a copy-through-pinned pipeline's DMA and page-cache
     # copies share host memory, so these contended rates are the context of save/restore
     cores = min(128, len(os.sched_getaffinity(0)))
-    per_rank = max(1, cores // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")) if d.on else 1))
+    local_world = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))) if d.on else 1
+    per_rank = max(1, cores // local_world)
     cdir = os.path.join(base, f"contended_{d.rank}")
     d.barrier()
     cw, cr, cd2h, ch2d = native.probe_storage_dma(cdir, per_rank, 1 << 30, 8 << 20, d.local if d.on else 0)
