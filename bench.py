@@ -1036,10 +1036,15 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
 
     cores = len(os.sched_getaffinity(0))
     P = processes or max(1, min(64, 1 << (cores.bit_length() - 1)))  # all host threads (power of 2)
-    dims = dict(LLAMA3_8B)
-    dims["layers"] = sample_layers
-    leaves = [(t, p, s, dt) for t, p, s, dt in llama_leaves(**dims)
-              if not p.startswith(("embed", "lm_head"))]
+    c1 = getattr(args, "config", "c2") == "c1"
+    if c1:  # BASELINE configs[0] itself: 4 x (4096, 4096) f32, unsharded, one process
+        P = 1
+        leaves = [("model", f"a{i}", (4096, 4096), "f32") for i in range(4)]
+    else:
+        dims = dict(LLAMA3_8B)
+        dims["layers"] = sample_layers
+        leaves = [(t, p, s, dt) for t, p, s, dt in llama_leaves(**dims)
+                  if not p.startswith(("embed", "lm_head"))]
     rng = np.random.default_rng(0)
     tree: dict = {"state": {}}
     specs: dict = {"state": {}}
@@ -1053,7 +1058,8 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
         else:
             data = rng.standard_normal(size=shape, dtype=np.float32)
         node[parts[-1]] = ("array", dt, data)
-        specs["state"][f"{t}/{p}"] = ([("fsdp", P)], P, None, ("fsdp",) + (None,) * (len(shape) - 1))
+        if not c1:
+            specs["state"][f"{t}/{p}"] = ([("fsdp", P)], P, None, ("fsdp",) + (None,) * (len(shape) - 1))
     sample_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
     root = os.path.join(root_dir or args.dir, "cpu_baseline")
     saves, restores = [], []
@@ -1086,9 +1092,11 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
         "unit": "GB/s",
         "cores": P,
         "kind": "port",
-        "sample": f"{sample_layers} transformer layers of the C2 tree (no embed/lm_head), "
-                  f"{sample_bytes} bytes, FSDP-{P} over {P} simulated processes (one host thread "
-                  f"each), save + restore per step, mean of {steps} after {warmup} warm-up",
+        "sample": (f"the whole C1 tree (4 x (4096,4096) f32, unsharded, one process), {sample_bytes} bytes"
+                   if c1 else
+                   f"{sample_layers} transformer layers of the C2 tree (no embed/lm_head), "
+                   f"{sample_bytes} bytes, FSDP-{P} over {P} simulated processes (one host thread each)")
+                  + f", save + restore per step, mean of {steps} after {warmup} warm-up",
         "save_GBps": round(sample_bytes / t_save / 1e9, 3),
         "restore_GBps": round(sample_bytes / t_restore / 1e9, 3),
     }
@@ -1115,8 +1123,9 @@ def run_reference(args) -> dict:
         "dtype": "u8",
         "payload_dtypes": "bf16 params + f32 Adam mu/nu, moved as bytes (no arithmetic on the path)",
         "data": "synthetic (numpy RNG, Llama-3-8B shapes)",
-        "config": {"workload": f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu (bounded sample: {res['sample']})",
-                   "config": "c2", "storage": f"oracle port writing/reading {args.dir} (tmpfs)"},
+        "config": {"workload": (f"C1: {res['sample']}" if args.config == "c1" else
+                                f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu (bounded sample: {res['sample']})"),
+                   "config": args.config, "storage": "oracle port on the same storage target as our arm"},
         "save_GBps": res["save_GBps"],
         "restore_GBps": res["restore_GBps"],
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
