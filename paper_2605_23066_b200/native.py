@@ -26,6 +26,7 @@ MAX_RANK = 8
 LIB_PATH = Path(__file__).resolve().parent / "libtvgpu.so"
 
 TV_OK = 0
+TV_ERR_IO = -2  # include/tvgpu.h
 
 # ---- C struct layouts -------------------------------------------------------------------
 
@@ -134,8 +135,16 @@ def last_error() -> str:
 
 
 def check(rc: int, what: str) -> None:
+    """Raise for a failed call: storage failures (open / pwrite / pread / rename / unlink,
+    TV_ERR_IO) as the reference's BackendError — the type its FilesystemBackend raises —
+    everything else (CUDA, arguments, memory) as NativeError."""
     if rc != TV_OK:
-        raise NativeError(f"{what} failed (code {rc}): {last_error()}")
+        msg = f"{what} failed (code {rc}): {last_error()}"
+        if rc == TV_ERR_IO:
+            from .errors import BackendError
+
+            raise BackendError(msg)
+        raise NativeError(msg)
 
 
 def require_gpu() -> None:
@@ -295,11 +304,8 @@ def unlink_many(paths: Sequence[str], threads: int) -> list[bool]:
         return []
     table = PathTable(list(paths))
     ok = np.zeros(len(paths), np.uint8)
-    rc = lib().tv_unlink_many(table.pointers.ctypes.data, len(paths), int(threads), ok.ctypes.data)
-    if rc != 0:
-        from .errors import BackendError
-
-        raise BackendError(last_error())
+    check(lib().tv_unlink_many(table.pointers.ctypes.data, len(paths), int(threads), ok.ctypes.data),
+          "tv_unlink_many")
     return [bool(x) for x in ok]
 
 
