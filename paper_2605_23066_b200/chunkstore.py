@@ -803,16 +803,16 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
             inputs[i]["size"] = arr.size
     for it in items:
         size = int(inputs[input_index[it.fetch.key]]["size"])
-        if it.fetch.file_off + it.fetch.nbytes > size:
+        if it.fetch.whole_file and size != it.fetch.nbytes:  # a per-leaf chunk object
+            raise CorruptionError(
+                f"chunk object {it.fetch.key!r} has {size} bytes, expected {it.fetch.nbytes}"
+            )
+        if it.fetch.file_off + it.fetch.nbytes > size:  # a span of an aggregated data file
             from .errors import BackendError
 
             raise BackendError(
                 f"range [{it.fetch.file_off}, {it.fetch.file_off + it.fetch.nbytes}) outside key "
                 f"{it.fetch.key!r} of size {size}"
-            )
-        if it.fetch.whole_file and size != it.fetch.nbytes:
-            raise CorruptionError(
-                f"chunk object {it.fetch.key!r} has {size} bytes, expected {it.fetch.nbytes}"
             )
     ritems = np.zeros(len(items), native.READ_ITEM)
     direct_dst = np.zeros(len(items), np.uint64)
