@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <errno.h>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <sys/types.h>
 #include <unistd.h>
@@ -444,6 +445,8 @@ struct tv_engine {
   int64_t staging_bytes;
   int n_threads;
   std::vector<char*> slots;  // pinned
+  char* ring = nullptr;       // one huge-page region holding every slot (TVGPU_HUGE_RING=1)
+  size_t ring_bytes = 0;
   std::mutex dev_m;
   std::map<int, std::unique_ptr<tv::DeviceCtx>> devices;
   std::mutex call_m;  // one save/load at a time per engine
@@ -1257,6 +1260,30 @@ int engine_create(int n_slots, int64_t slot_bytes, int64_t staging_bytes, int n_
   e->slot_bytes = slot_bytes;
   e->staging_bytes = std::max<int64_t>(staging_bytes, (int64_t)n_slots * slot_bytes);
   e->n_threads = n_threads;
+  const char* huge = std::getenv("TVGPU_HUGE_RING");
+  if (huge && std::atoi(huge) != 0) {
+    // One 2 MiB-page region (THP via madvise), faulted in, then pinned: fewer TLB entries
+    // for both the writers' reads and the copy engine's accesses.
+    const size_t hp = 2u << 20;
+    e->ring_bytes = (((size_t)n_slots * (size_t)slot_bytes) + hp - 1) / hp * hp;
+    void* m = mmap(nullptr, e->ring_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (m == MAP_FAILED) {
+      set_error("mmap of the huge-page slot ring failed");
+      return TV_ERR_NOMEM;
+    }
+    madvise(m, e->ring_bytes, MADV_HUGEPAGE);
+    std::memset(m, 0, e->ring_bytes);
+    cudaError_t ce = cudaHostRegister(m, e->ring_bytes, cudaHostRegisterPortable);
+    if (ce != cudaSuccess) {
+      munmap(m, e->ring_bytes);
+      set_error(std::string("cudaHostRegister(slot ring): ") + cudaGetErrorString(ce));
+      return TV_ERR_NOMEM;
+    }
+    e->ring = static_cast<char*>(m);
+    for (int i = 0; i < n_slots; ++i) e->slots.push_back(e->ring + (size_t)i * slot_bytes);
+    *out = e.release();
+    return TV_OK;
+  }
   for (int i = 0; i < n_slots; ++i) {
     char* p = nullptr;
     cudaError_t ce = cudaHostAlloc(&p, slot_bytes, cudaHostAllocPortable);
@@ -1284,7 +1311,12 @@ int engine_destroy(tv_engine* e) {
     }
     e->devices.clear();
   }
-  for (auto p : e->slots) cudaFreeHost(p);
+  if (e->ring) {
+    cudaHostUnregister(e->ring);
+    munmap(e->ring, e->ring_bytes);
+  } else {
+    for (auto p : e->slots) cudaFreeHost(p);
+  }
   delete e;
   return TV_OK;
 }
