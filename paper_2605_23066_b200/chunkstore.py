@@ -638,8 +638,18 @@ def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMet
     (``chunkstore.py:507-578``): per covering write chunk, the whole chunk when every
     subchunk is needed or subchunks are not contiguous in it, else one byte-range fetch
     per needed subchunk."""
-    w, r = meta.write_chunk, meta.read_chunk
-    isz = itemsize(meta.dtype)
+    geometry = fetch_geometry(meta.write_chunk, meta.read_chunk, itemsize(meta.dtype),
+                              tuple(tuple(r_) for r_ in requests))
+    return fetches_at(prefix, leaf_path, entry, geometry)
+
+
+@functools.lru_cache(maxsize=1 << 12)
+def fetch_geometry(w: tuple[int, ...], r: tuple[int, ...], isz: int,
+                   requests: tuple[tuple[Range, ...], ...]) -> tuple[tuple, ...]:
+    """The storage-independent part of ``plan_fetches``: per fetch ``(chunk key, byte
+    offset in the chunk, nbytes, origin, shape, whole chunk)``.  A pure function of the
+    chunk grid and the requested boxes, so the leaves of a tree that share a shape and
+    sharding (every layer of a transformer) share one entry."""
     subs_per = tuple(wi // ri for wi, ri in zip(w, r))
     n_subs = math.prod(subs_per)
     contiguous = _slab_is_contiguous(r, w)
@@ -647,7 +657,7 @@ def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMet
     chunks: dict[tuple[int, ...], set[tuple[int, ...]] | None] = {}
     order: list[tuple[int, ...]] = []
     whole_only = n_subs == 1  # read chunk == write chunk: every covering chunk is read whole
-    for ranges in dict.fromkeys(tuple(r_) for r_ in requests):  # replicas ask for the same box
+    for ranges in dict.fromkeys(requests):  # replicas ask for the same box
         if any(e == 0 for _, e in ranges):
             continue
         for coords in _covering(ranges, w):
@@ -664,32 +674,45 @@ def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMet
                 subs = chunks[coords] = set()
                 order.append(coords)
             subs.update(_covering(hit, r))
-    locations = entry["chunks"]
-    out: list[Fetch] = []
+    out: list[tuple] = []
     chunk_bytes = math.prod(w) * isz
     sub_bytes = math.prod(r) * isz
     for coords in order:
         ck = coords_key(coords)
-        loc = locations.get(ck)
-        if loc is None:
-            raise CorruptionError(f"chunk {ck} of {leaf_path!r} missing from merged index")
-        if "f" in loc:
-            key = f"{prefix}/process_{loc['p']}/{DATA_DIR}/{loc['f']}"
-            base, op, whole = int(loc["o"]), "get_range", False
-        else:
-            key = f"{prefix}/process_{loc['p']}/" + chunk_object_key(leaf_path, coords)
-            base, op, whole = 0, "get", True
         needed = chunks[coords]
-        origin = tuple(c * wi for c, wi in zip(coords, w))
         if whole_only or len(needed) == n_subs or not contiguous:
-            out.append(Fetch(key, op, base, chunk_bytes, origin, tuple(w), whole))
+            out.append((coords, ck, 0, chunk_bytes, tuple(c * wi for c, wi in zip(coords, w)),
+                        tuple(w), True))
             continue
         for sub in sorted(needed):
             rel = tuple(s - c * n for s, c, n in zip(sub, coords, subs_per))
             first = sum(rc * ri * st for rc, ri, st in zip(rel, r, wstrides))
-            sub_origin = tuple(s * ri for s, ri in zip(sub, r))
-            out.append(Fetch(key, "get_range", base + first * isz, sub_bytes, sub_origin,
-                             tuple(r), False))
+            out.append((coords, ck, first * isz, sub_bytes, tuple(s * ri for s, ri in zip(sub, r)),
+                        tuple(r), False))
+    return tuple(out)
+
+
+def fetches_at(prefix: str, leaf_path: str, entry: dict, geometry: tuple[tuple, ...]) -> list[Fetch]:
+    """Bind a fetch geometry to one leaf's stored chunks (merged-index locations)."""
+    locations = entry["chunks"]
+    out: list[Fetch] = []
+    bound: tuple = ()
+    for coords, ck, rel, nbytes, origin, shape, whole_chunk in geometry:
+        if not bound or bound[0] != ck:
+            loc = locations.get(ck)
+            if loc is None:
+                raise CorruptionError(f"chunk {ck} of {leaf_path!r} missing from merged index")
+            if "f" in loc:
+                key = f"{prefix}/process_{loc['p']}/{DATA_DIR}/{loc['f']}"
+                bound = (ck, key, int(loc["o"]), "get_range", False)
+            else:
+                key = f"{prefix}/process_{loc['p']}/" + chunk_object_key(leaf_path, coords)
+                bound = (ck, key, 0, "get", True)
+        _, key, base, op, whole = bound
+        if whole_chunk:
+            out.append(Fetch(key, op, base, nbytes, origin, shape, whole))
+        else:
+            out.append(Fetch(key, "get_range", base + rel, nbytes, origin, shape, False))
     return out
 
 

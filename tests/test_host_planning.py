@@ -214,3 +214,46 @@ def test_box_index_matches_linear_scan():
             q = tuple(q)
             expect = [i for i, b in enumerate(boxes) if cs._intersect(q, b) is not None]
             assert index.hits(q) == expect, (boxes, q)
+
+
+def test_memoised_fetch_and_consumer_geometry():
+    """The memoised fetch geometry bound to a leaf gives the same fetches as planning it
+    from scratch, and the cached consumer geometry names exactly the boxes each fetch
+    meets and, among them, those it lands in as one contiguous run."""
+    import random
+
+    from paper_2605_23066_b200 import chunkstore as cs
+    from paper_2605_23066_b200 import load_pipeline as lp
+
+    rng = random.Random(11)
+    for case in range(200):
+        rank = rng.randint(1, 3)
+        w = tuple(rng.choice([2, 4, 8]) for _ in range(rank))
+        r = tuple(wi // rng.choice([d for d in (1, 2, 4) if wi % d == 0]) for wi in w)
+        g = tuple(wi * rng.randint(1, 3) for wi in w)
+        meta = cs.ArrayStorageMetadata(g, "f32", g, w, r, "per_leaf")
+        entry = {"chunks": {cs.coords_key(c): {"p": 0} for c in cs._covering(tuple((0, e) for e in g), w)}}
+        reqs = []
+        for _ in range(rng.randint(1, 4)):
+            b = []
+            for e in g:
+                o = rng.randint(0, e - 1)
+                b.append((o, rng.randint(1, e - o)))
+            reqs.append(tuple(b))
+        fetches = cs.plan_fetches("ck", f"t/l{case}", entry, meta, reqs)
+        geometry = cs.fetch_geometry(w, r, 4, tuple(reqs))
+        assert cs.fetches_at("ck", f"t/l{case}", entry, geometry) == fetches
+        for f in fetches:
+            assert f.key.startswith(f"ck/process_0/t/l{case}/c.")
+        for f, (hits, direct) in zip(fetches, lp._consumer_geometry(geometry, tuple(reqs))):
+            box = tuple(zip(f.origin, f.shape))
+            assert list(hits) == [i for i, b in enumerate(reqs) if cs._intersect(box, b) is not None]
+            expect = []
+            for i in hits:
+                b = reqs[i]
+                inside = all(to <= bo and bo + be <= to + te for (bo, be), (to, te) in zip(box, b))
+                if inside and cs.box_is_contiguous(tuple(e for _, e in b),
+                                                   tuple(bo - to for (bo, _), (to, _) in zip(box, b)),
+                                                   f.shape):
+                    expect.append(i)
+            assert list(direct) == expect
