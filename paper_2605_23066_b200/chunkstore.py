@@ -338,7 +338,7 @@ class AggregatedManifest:
 # -- device regions ---------------------------------------------------------------------
 
 
-@dataclass
+@dataclass(slots=True)
 class DeviceRegion:
     """Where the values of one box live on a GPU: the contiguous row-major array at
     ``address`` of extents ``shape`` holds the box at offset ``origin``.  A shard, a
@@ -396,7 +396,7 @@ def _fill_box(rec: np.ndarray, base: int, shape: Sequence[int], off: Sequence[in
 # -- writer ---------------------------------------------------------------------------------
 
 
-@dataclass
+@dataclass(slots=True)
 class _PendingChunk:
     key: str          # full storage key of the output (chunk object, or data file)
     region: DeviceRegion
@@ -619,7 +619,7 @@ class ReadStats:
     bytes_loaded: int = 0
 
 
-@dataclass
+@dataclass(slots=True)
 class Fetch:
     """One contiguous byte range of a stored chunk and the box it holds."""
 
@@ -764,7 +764,7 @@ class ChunkReader:
 # -- restore execution ------------------------------------------------------------------------
 
 
-@dataclass
+@dataclass(slots=True)
 class Destination:
     """A target box on a GPU: the tensor at ``address`` holds global box ``ranges``.
     ``src_code``/``dst_code`` (native.DTYPE_CODE) make the copy into it converting (the
@@ -779,7 +779,7 @@ class Destination:
     src_itemsize: int = 0
 
 
-@dataclass
+@dataclass(slots=True)
 class FetchItem:
     fetch: Fetch
     reader_gpu: int
