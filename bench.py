@@ -504,11 +504,27 @@ def run_ours(args) -> dict:
     gc_ms = [0.0, 0, 0]  # time, collections, gen-2 collections in the timed steps (this rank)
     gc_t0 = [0.0]
 
+    gc_sources: dict[str, list] = {}  # TVGPU_GC_SOURCES=1: where collections are triggered
+    trace_gc = os.environ.get("TVGPU_GC_SOURCES") == "1"
+
     def _gc_cb(phase, info):
         if phase == "start":
             gc_t0[0] = time.perf_counter()
+            if trace_gc:
+                import traceback
+
+                ours = [f for f in traceback.extract_stack()[:-1]
+                        if "paper_2605_23066_b200" in f.filename or f.filename.endswith("bench.py")]
+                if ours:
+                    f = ours[-1]
+                    site = f"{os.path.basename(f.filename)}:{f.lineno} {f.name}"
+                    gc_sources.setdefault(site, [0, 0.0])[0] += 1
+                    gc_t0.append(site)
         else:
-            gc_ms[0] += (time.perf_counter() - gc_t0[0]) * 1e3
+            dt_ms = (time.perf_counter() - gc_t0[0]) * 1e3
+            gc_ms[0] += dt_ms
+            if len(gc_t0) > 1:
+                gc_sources[gc_t0.pop()][1] += dt_ms
             gc_ms[1] += 1
             gc_ms[2] += int(info.get("generation") == 2)
 
@@ -636,7 +652,9 @@ def run_ours(args) -> dict:
         "engine_rank0": engine,
         "phases_ms_rank0_last_step": phases,
         "python_gc_rank0": {"ms_per_step": round(gc_ms[0] / args.steps, 2),
-                            "collections": gc_ms[1], "gen2": gc_ms[2]},
+                            "collections": gc_ms[1], "gen2": gc_ms[2],
+                            **({"sources": sorted(([k, n, round(t, 2)] for k, (n, t) in gc_sources.items()),
+                                                  key=lambda x: -x[2])[:25]} if trace_gc else {})},
         "restore_verified": dict(verified, how="after the timed steps: every restored shard's overlap "
                                                "with every saved shard compared with torch.equal on "
                                                "the device (all ranks)"),
