@@ -364,6 +364,21 @@ def open_runtime(tv, d, N, backend, gpus=None):
     return tv.SimulatedRuntime(N, backend, gpus=gpus)
 
 
+def _numa_nodes() -> int:
+    import glob
+
+    from paper_2605_23066_b200 import native
+
+    n = 0
+    for node in glob.glob("/sys/devices/system/node/node[0-9]*"):
+        try:
+            with open(f"{node}/cpulist") as f:
+                n += bool(native.parse_cpulist(f.read()))
+        except OSError:
+            pass
+    return n
+
+
 def run_ours(args) -> dict:
     import torch
 
@@ -650,6 +665,9 @@ def run_ours(args) -> dict:
         },
         "clocks": clock_info,
         "engine_rank0": engine,
+        "numa_rank0": {"nodes_with_cpus": _numa_nodes(), **native.placement(),
+                       "note": "storage threads + pinned ring bound to the GPU's local CPUs "
+                               "when the host has > 1 NUMA node (torchrun); {} = not placed"},
         "phases_ms_rank0_last_step": phases,
         "python_gc_rank0": {"ms_per_step": round(gc_ms[0] / args.steps, 2),
                             "collections": gc_ms[1], "gen2": gc_ms[2],

@@ -360,6 +360,7 @@ class Engine:
 
     def __init__(self, n_slots: int, slot_bytes: int, staging_bytes: int, threads: int):
         self.config = (n_slots, slot_bytes, staging_bytes, threads)
+        self.cpus: set[int] | None = None  # NUMA placement of its threads (_create_engine)
         handle = ctypes.c_void_p()
         check(lib().tv_engine_create(n_slots, slot_bytes, staging_bytes, threads,
                                      ctypes.byref(handle)), "tv_engine_create")
@@ -374,8 +375,9 @@ class Engine:
         stats = np.zeros(1, STATS)
         items = np.ascontiguousarray(items, WRITE_ITEM)
         outputs = np.ascontiguousarray(outputs, OUTPUT)
-        rc = lib().tv_engine_save(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
-                                  stats.ctypes.data)
+        with _bound_to(self.cpus):
+            rc = lib().tv_engine_save(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
+                                      stats.ctypes.data)
         _account("save", stats[0])
         check(rc, "tv_engine_save")
         return stats[0]
@@ -385,8 +387,9 @@ class Engine:
         items = np.ascontiguousarray(items, READ_ITEM)
         inputs = np.ascontiguousarray(inputs, INPUT)
         copies = np.ascontiguousarray(copies, COPY)
-        rc = lib().tv_engine_load(self._h, _ptr(items), len(items), _ptr(inputs), len(inputs),
-                                  _ptr(copies), len(copies), stats.ctypes.data)
+        with _bound_to(self.cpus):
+            rc = lib().tv_engine_load(self._h, _ptr(items), len(items), _ptr(inputs), len(inputs),
+                                      _ptr(copies), len(copies), stats.ctypes.data)
         _account("load", stats[0])
         check(rc, "tv_engine_load")
         return stats[0]
@@ -472,6 +475,109 @@ class EngineConfig:
         return n_slots, slot, staging, threads
 
 
+def parse_cpulist(text: str) -> set[int]:
+    """Linux cpulist syntax ("0-3,8,10-11") -> CPU ids."""
+    out: set[int] = set()
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        lo, _, hi = part.partition("-")
+        out.update(range(int(lo), int(hi or lo) + 1))
+    return out
+
+
+def numa_local_cpus(pci_address: str, sysfs: str = "/sys", force: bool = False) -> set[int] | None:
+    """CPUs of the NUMA node a PCI device (the GPU) hangs off, when the host has more than
+    one node with CPUs — else None (one node: nothing to place; ``force`` places anyway,
+    for testing the path on single-node boxes)."""
+    import glob
+
+    nodes = 0
+    for node in glob.glob(f"{sysfs}/devices/system/node/node[0-9]*"):
+        try:
+            with open(f"{node}/cpulist") as f:
+                nodes += bool(parse_cpulist(f.read()))
+        except OSError:
+            continue
+    if nodes < 2 and not force:
+        return None
+    try:
+        with open(f"{sysfs}/bus/pci/devices/{pci_address}/local_cpulist") as f:
+            cpus = parse_cpulist(f.read())
+    except (OSError, ValueError):
+        return None
+    return cpus or None
+
+
+_placement: dict = {}
+
+
+def _engine_cpus() -> set[int] | None:
+    """Where a new engine's storage threads and pinned ring go: the CPUs local to this
+    rank's GPU under torchrun (one GPU per rank, LOCAL_WORLD_SIZE > 1) on multi-node
+    hosts, intersected with the process's allowed CPUs.  TVGPU_NUMA=0 disables,
+    TVGPU_NUMA=force applies it on single-node hosts too."""
+    mode = os.environ.get("TVGPU_NUMA", "auto")
+    if mode == "0" or not hasattr(os, "sched_setaffinity"):
+        return None
+    if mode != "force" and int(os.environ.get("LOCAL_WORLD_SIZE", "1")) <= 1:
+        return None
+    import torch
+
+    def local_of(gpu: int) -> set[int] | None:
+        prop = torch.cuda.get_device_properties(gpu)
+        addr = f"{prop.pci_domain_id:04x}:{prop.pci_bus_id:02x}:{prop.pci_device_id:02x}.0"
+        return numa_local_cpus(addr, force=mode == "force")
+
+    gpu = torch.cuda.current_device()
+    local = local_of(gpu)
+    if local is None:
+        return None
+    allowed = os.sched_getaffinity(0)
+    cpus = local & allowed
+    # Bind only when this node's share of the local ranks' GPUs does not exceed its share
+    # of the CPUs (the per-engine thread count assumes an even split of the host's cores).
+    ranks = min(int(os.environ.get("LOCAL_WORLD_SIZE", "1")), torch.cuda.device_count())
+    same = sum(1 for g in range(ranks) if local_of(g) == local) or 1
+    if not cpus or same * len(allowed) > len(cpus) * max(ranks, 1) * 1.01:
+        return None
+    _placement.update({"gpu": gpu, "cpus": len(cpus), "ranks_on_node": same})
+    return cpus
+
+
+def placement() -> dict:
+    """The NUMA placement applied to this process's engines ({} when none)."""
+    return dict(_placement)
+
+
+class _bound_to:
+    """Run the calling thread on ``cpus`` for the duration (no-op for None).  Threads it
+    starts inherit the mask (the engine's storage threads are started per operation)."""
+
+    def __init__(self, cpus: set[int] | None):
+        self.cpus, self.before = cpus, None
+
+    def __enter__(self):
+        if self.cpus is not None:
+            self.before = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, self.cpus)
+
+    def __exit__(self, *exc):
+        if self.before is not None:
+            os.sched_setaffinity(0, self.before)
+            self.before = None
+
+
+def _create_engine(key: tuple) -> Engine:
+    """Create an engine bound to the GPU's local CPUs (when placed): its pinned ring is
+    allocated, and its storage threads run and fill the page cache, on the GPU's node."""
+    cpus = _engine_cpus()
+    with _bound_to(cpus):
+        engine = Engine(*key)
+    engine.cpus = cpus
+    return engine
+
+
 _pool: dict[tuple, list[Engine]] = {}
 _pool_lock = threading.Lock()
 
@@ -489,7 +595,7 @@ class engine_lease:
             idle = _pool.setdefault(self.key, [])
             self.engine = idle.pop() if idle else None
         if self.engine is None:
-            self.engine = Engine(*self.key)
+            self.engine = _create_engine(self.key)
         return self.engine
 
     def __exit__(self, *exc) -> None:

@@ -257,3 +257,40 @@ def test_memoised_fetch_and_consumer_geometry():
                                                    f.shape):
                     expect.append(i)
             assert list(direct) == expect
+
+
+def test_numa_cpu_placement_from_sysfs(tmp_path):
+    """The GPU's local CPUs come from its PCI device's local_cpulist, and only when the
+    host has more than one NUMA node with CPUs (force: always)."""
+    from paper_2605_23066_b200 import native
+
+    assert native.parse_cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert native.parse_cpulist("") == set()
+    nodes = tmp_path / "devices" / "system" / "node"
+    (nodes / "node0").mkdir(parents=True)
+    (nodes / "node0" / "cpulist").write_text("0-15\n")
+    dev = tmp_path / "bus" / "pci" / "devices" / "0000:1b:00.0"
+    dev.mkdir(parents=True)
+    (dev / "local_cpulist").write_text("16-31\n")
+    assert native.numa_local_cpus("0000:1b:00.0", sysfs=str(tmp_path)) is None  # one node
+    assert native.numa_local_cpus("0000:1b:00.0", sysfs=str(tmp_path), force=True) == set(range(16, 32))
+    (nodes / "node1").mkdir()
+    (nodes / "node1" / "cpulist").write_text("16-31\n")
+    (nodes / "node2").mkdir()  # memory-only node: no CPUs
+    (nodes / "node2" / "cpulist").write_text("\n")
+    assert native.numa_local_cpus("0000:1b:00.0", sysfs=str(tmp_path)) == set(range(16, 32))
+    assert native.numa_local_cpus("0000:99:00.0", sysfs=str(tmp_path)) is None  # unknown device
+
+
+def test_bound_to_restores_affinity():
+    import os
+
+    from paper_2605_23066_b200 import native
+
+    before = os.sched_getaffinity(0)
+    one = {min(before)}
+    with native._bound_to(one):
+        assert os.sched_getaffinity(0) == one
+    assert os.sched_getaffinity(0) == before
+    with native._bound_to(None):
+        assert os.sched_getaffinity(0) == before
