@@ -563,6 +563,18 @@ def run_ours(args) -> dict:
     me = d.rank if d.on else 0
     phases = {"save": dict(timeline.LAST_SAVE.get(me, {})),
               "restore": {**timeline.LAST_RESTORE.get(me, {}), **timeline.LAST_RESTORE.get(-1, {})}}
+    # rank skew: each process's own write phase / engine load in the last step
+    mine = {p: [round(ph.get("write_phase", 0.0), 1),
+                round(timeline.LAST_RESTORE.get(p, {}).get("engine_load", 0.0), 1)]
+            for p, ph in timeline.LAST_SAVE.items()}
+    if d.on:
+        import torch.distributed as dist
+
+        every = [None] * d.world
+        dist.all_gather_object(every, {me: mine.get(me, [0.0, 0.0])})
+        mine = {k: v for part in every for k, v in part.items()}
+    skew = {"write_phase_ms": [mine[p][0] for p in sorted(mine)],
+            "engine_load_ms": [mine[p][1] for p in sorted(mine)]}
     after = native.totals()
     clock_info = clocks.stop() if d.rank == 0 else {}
     kernels = d.sum(after["kernel_launches"] - before["kernel_launches"])
@@ -669,6 +681,7 @@ def run_ours(args) -> dict:
                        "note": "storage threads + pinned ring bound to the GPU's local CPUs "
                                "when the host has > 1 NUMA node (torchrun); {} = not placed"},
         "phases_ms_rank0_last_step": phases,
+        "per_process_last_step": skew,
         "python_gc_rank0": {"ms_per_step": round(gc_ms[0] / args.steps, 2),
                             "collections": gc_ms[1], "gen2": gc_ms[2],
                             **({"sources": sorted(([k, n, round(t, 2)] for k, (n, t) in gc_sources.items()),
