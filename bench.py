@@ -72,15 +72,35 @@ def nbytes(shape, dtype) -> int:
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled every 200 ms (rank 0)."""
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms (rank 0), on the GPUs
+    the job uses only: nvidia-smi ignores CUDA_VISIBLE_DEVICES, and idle neighbours on a
+    larger box would drag the median toward their idle clock.  GPUs are matched by PCI
+    address (some boxes redact nvidia-smi's UUIDs)."""
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    QUERY = ("pci.bus_id,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self):
+    def __init__(self, n_devices: int = 1):
         self.proc = None
         self.path = tempfile.mktemp(prefix="tv_clocks_", suffix=".csv")
+        self.buses = set()
+        try:
+            import torch
+            for i in range(min(max(1, n_devices), torch.cuda.device_count())):
+                pr = torch.cuda.get_device_properties(i)
+                self.buses.add((pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id))
+        except Exception:
+            self.buses = set()
+
+    @staticmethod
+    def _bus(text: str):
+        """"00000000:D1:00.0" -> (domain, bus, device)."""
+        try:
+            dom, bus, dev = text.split(".")[0].split(":")
+            return int(dom, 16), int(bus, 16), int(dev, 16)
+        except ValueError:
+            return None
 
     def start(self):
         if shutil.which("nvidia-smi") is None:
@@ -96,10 +116,14 @@ class ClockSampler:
         self.proc.terminate()
         self.proc.wait()
         self.f.close()
+        rows = [[p.strip() for p in line.split(",")] for line in open(self.path)]
+        mine = [r for r in rows if len(r) >= 9 and self._bus(r[0]) in self.buses]
+        if not mine:  # PCI addresses unresolved: sample every GPU on the box
+            self.buses = set()
+            mine = rows
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
+        for parts in mine:
             if len(parts) < 9:
                 continue
             try:
@@ -116,6 +140,7 @@ class ClockSampler:
             "sm_max_mhz": max(smax) if smax else None,
             "reasons": sorted(reasons),
             "samples": len(sm),
+            "gpus_sampled": len(self.buses) or "all",
         }
 
 
@@ -511,7 +536,7 @@ def run_ours(args) -> dict:
                         "thread loops 64 MiB D2H (during writes) / H2D (during reads) on its GPU; summed"}
     d.barrier()
 
-    clocks = ClockSampler()
+    clocks = ClockSampler(max(N, args.restore_gpus or 0))
     if d.rank == 0:
         clocks.start()
     import gc
