@@ -748,6 +748,27 @@ def run_ours(args) -> dict:
     return result
 
 
+def _storage_room(path: str):
+    """Bytes the storage under `path` can take: free space, capped by available host RAM
+    when the filesystem is RAM-backed (tmpfs)."""
+    try:
+        st = os.statvfs(path)
+        free = st.f_bavail * st.f_frsize
+        fstype = ""
+        best = ""
+        for line in open("/proc/mounts"):
+            dev, mnt, typ = line.split()[:3]
+            if os.path.realpath(path).startswith(mnt.rstrip("/") + "/") and len(mnt) > len(best):
+                best, fstype = mnt, typ
+        if fstype in ("tmpfs", "ramfs"):
+            for line in open("/proc/meminfo"):
+                if line.startswith("MemAvailable:"):
+                    free = min(free, int(line.split()[1]) * 1024)
+        return free
+    except (OSError, ValueError):
+        return None
+
+
 def run_c5(args) -> dict:
     """C5: Checkpointer async save every step (keep_last=3) inside a synthetic training
     loop; reports the time the training loop is blocked in save_step."""
@@ -769,6 +790,12 @@ def run_c5(args) -> dict:
     rt = open_runtime(tv, d, N, backend, gpus=list(range(N)))
     leaves = llama_leaves(**dict(LLAMA3_8B, layers=args.layers))
     tree_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
+    # keep_last=3 plus the save in flight live on the storage at once; on a RAM-backed
+    # target that must fit host memory, or the kernel OOM-kills the job mid-save
+    need, room = 4 * tree_bytes, _storage_room(base)
+    if room is not None and need > room:
+        raise SystemExit(f"c5: {need / 1e9:.1f} GB of checkpoints (keep_last=3 + 1 in flight) do not fit "
+                         f"the {room / 1e9:.1f} GB free on {base}; pass --layers to shrink the tree")
     state, shardings = build_state(tv, rt, mesh, leaves)
     params = [t for p, leaf in tv.flatten(state["state"]["params"]) for t in leaf.shards.values()]
     torch.cuda.synchronize()
