@@ -628,8 +628,9 @@ class Fetch:
     file_off: int
     nbytes: int
     origin: tuple[int, ...]       # global origin of the fetched box
-    shape: tuple[int, ...]        # box shape (write chunk or read chunk)
+    shape: tuple[int, ...]        # box shape (write chunk, read chunk, or a slab of one)
     whole_file: bool
+    object_bytes: int = -1        # size a per-leaf chunk object must have (-1: no check)
 
 
 def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMetadata,
@@ -646,10 +647,12 @@ def plan_fetches(prefix: str, leaf_path: str, entry: dict, meta: ArrayStorageMet
 @functools.lru_cache(maxsize=1 << 12)
 def fetch_geometry(w: tuple[int, ...], r: tuple[int, ...], isz: int,
                    requests: tuple[tuple[Range, ...], ...]) -> tuple[tuple, ...]:
-    """The storage-independent part of ``plan_fetches``: per fetch ``(chunk key, byte
-    offset in the chunk, nbytes, origin, shape, whole chunk)``.  A pure function of the
-    chunk grid and the requested boxes, so the leaves of a tree that share a shape and
-    sharding (every layer of a transformer) share one entry."""
+    """The storage-independent part of ``plan_fetches``: per fetch ``(chunk coords, chunk
+    key, byte offset in the chunk, nbytes, origin, shape, whole chunk, object bytes)``
+    where object bytes is the size a per-leaf chunk object read whole must have (-1 for
+    subchunk spans).  A pure function of the chunk grid and the requested boxes, so the
+    leaves of a tree that share a shape and sharding (every layer of a transformer) share
+    one entry."""
     subs_per = tuple(wi // ri for wi, ri in zip(w, r))
     n_subs = math.prod(subs_per)
     contiguous = _slab_is_contiguous(r, w)
@@ -682,14 +685,127 @@ def fetch_geometry(w: tuple[int, ...], r: tuple[int, ...], isz: int,
         needed = chunks[coords]
         if whole_only or len(needed) == n_subs or not contiguous:
             out.append((coords, ck, 0, chunk_bytes, tuple(c * wi for c, wi in zip(coords, w)),
-                        tuple(w), True))
+                        tuple(w), True, chunk_bytes))
             continue
         for sub in sorted(needed):
             rel = tuple(s - c * n for s, c, n in zip(sub, coords, subs_per))
             first = sum(rc * ri * st for rc, ri, st in zip(rel, r, wstrides))
             out.append((coords, ck, first * isz, sub_bytes, tuple(s * ri for s, ri in zip(sub, r)),
-                        tuple(r), False))
+                        tuple(r), False, -1))
     return tuple(out)
+
+
+# -- restore fetch splitting ------------------------------------------------------------------
+#
+# The reference assembles any target box from whole chunks in host memory, with no size
+# ceiling (``chunkstore.py:507-593``).  Here a fetch that does not land contiguously in its
+# reader's target goes through device staging, which is bounded.  A fetched box is stored
+# row-major and contiguous, so a slab of it along its leading (first non-unit) dimension
+# is itself one contiguous byte range of the stored chunk: fetches are cut into such
+# slabs — at the target boxes' boundaries first, so each piece can land directly (H2D,
+# no kernel, no NVLink hop) in the one target that holds it, then into slabs of at most
+# the staging budget.  Every stored byte a target needs is still read exactly once.
+
+
+def _leading_dim(shape: Sequence[int]) -> int | None:
+    for d, e in enumerate(shape):
+        if e > 1:
+            return d
+    return None
+
+
+def _slab(rel: int, origin: tuple[int, ...], shape: tuple[int, ...], d: int, a: int, b: int,
+          row: int) -> tuple[int, int, tuple[int, ...], tuple[int, ...]]:
+    """(byte offset, nbytes, origin, shape) of rows [a, b) along dim ``d`` of a box whose
+    dims before ``d`` have extent 1 (``row`` = bytes per index of dim ``d``)."""
+    o = list(origin)
+    s = list(shape)
+    o[d] += a
+    s[d] = b - a
+    return rel + a * row, (b - a) * row, tuple(o), tuple(s)
+
+
+def cut_rows(rel: int, nbytes: int, origin: tuple[int, ...], shape: tuple[int, ...],
+             max_bytes: int) -> list[tuple[int, int, tuple[int, ...], tuple[int, ...]]]:
+    """Cut a contiguous box into consecutive contiguous slabs of at most ``max_bytes``
+    (descending into the next dimension when one index of the leading one is larger)."""
+    if nbytes <= max_bytes:
+        return [(rel, nbytes, origin, shape)]
+    d = _leading_dim(shape)
+    if d is None:  # one element larger than the budget: nothing to cut
+        return [(rel, nbytes, origin, shape)]
+    row = nbytes // shape[d]
+    if row <= max_bytes:
+        per = max(1, max_bytes // row)
+        return [_slab(rel, origin, shape, d, a, min(a + per, shape[d]), row)
+                for a in range(0, shape[d], per)]
+    out = []
+    for a in range(shape[d]):
+        out.extend(cut_rows(*_slab(rel, origin, shape, d, a, a + 1, row), max_bytes))
+    return out
+
+
+def _lands_contiguously(box: tuple[Range, ...], target: tuple[Range, ...]) -> bool:
+    if not all(to <= bo and bo + be <= to + te for (bo, be), (to, te) in zip(box, target)):
+        return False
+    return box_is_contiguous(tuple(e for _, e in target),
+                             tuple(bo - to for (bo, _), (to, _) in zip(box, target)),
+                             tuple(e for _, e in box))
+
+
+@functools.lru_cache(maxsize=1 << 12)
+def split_geometry(geometry: tuple[tuple, ...], boxes: tuple[tuple[Range, ...], ...],
+                   max_bytes: int) -> tuple[tuple, ...]:
+    """Refine a restore's fetch geometry (see above): a fetch no target box holds as one
+    contiguous run is cut along its leading dimension at the target boxes' boundaries;
+    pieces no target needs are dropped; pieces that still land contiguously nowhere are
+    cut into slabs of at most ``max_bytes``.  Fetches some target holds contiguously are
+    kept whole (they land there directly; replicas are served from the landing copy)."""
+    index = BoxIndex(boxes)
+    out: list[tuple] = []
+    for g in geometry:
+        coords, ck, rel, nbytes, origin, shape, whole, obj = g
+        box = tuple(zip(origin, shape))
+        hits = index.hits(box)
+        if any(_lands_contiguously(box, boxes[i]) for i in hits):
+            out.append(g)
+            continue
+        d = _leading_dim(shape)
+        pieces = [(rel, nbytes, origin, shape)]
+        if d is not None:
+            cuts = {0, shape[d]}
+            for i in hits:
+                o, e = boxes[i][d]
+                for c in (o - origin[d], o + e - origin[d]):
+                    if 0 < c < shape[d]:
+                        cuts.add(c)
+            row = nbytes // shape[d]
+            cuts_sorted = sorted(cuts)
+            pieces = [_slab(rel, origin, shape, d, a, b, row) for a, b in zip(cuts_sorted, cuts_sorted[1:])]
+        for prel, pbytes, porigin, pshape in pieces:
+            pbox = tuple(zip(porigin, pshape))
+            phits = index.hits(pbox)
+            if not phits:
+                continue  # bytes no target needs are not read
+            if any(_lands_contiguously(pbox, boxes[i]) for i in phits):
+                out.append((coords, ck, prel, pbytes, porigin, pshape, whole and pbytes == nbytes, obj))
+                continue
+            for srel, sbytes, sorigin, sshape in cut_rows(prel, pbytes, porigin, pshape, max_bytes):
+                if not index.hits(tuple(zip(sorigin, sshape))):
+                    continue
+                out.append((coords, ck, srel, sbytes, sorigin, sshape, whole and sbytes == nbytes, obj))
+    return tuple(out)
+
+
+def split_fetch(f: Fetch, max_bytes: int) -> list[Fetch]:
+    """``f`` as consecutive contiguous slabs of at most ``max_bytes`` (execution-time
+    guard for fetches that would need more device staging than the budget)."""
+    if f.nbytes <= max_bytes:
+        return [f]
+    pieces = cut_rows(f.file_off, f.nbytes, f.origin, f.shape, max_bytes)
+    if len(pieces) == 1:
+        return [f]
+    return [Fetch(f.key, "get_range", off, n, o, s, False, f.object_bytes) for off, n, o, s in pieces]
 
 
 def fetches_at(prefix: str, leaf_path: str, entry: dict, geometry: tuple[tuple, ...]) -> list[Fetch]:
@@ -697,7 +813,7 @@ def fetches_at(prefix: str, leaf_path: str, entry: dict, geometry: tuple[tuple, 
     locations = entry["chunks"]
     out: list[Fetch] = []
     bound: tuple = ()
-    for coords, ck, rel, nbytes, origin, shape, whole_chunk in geometry:
+    for coords, ck, rel, nbytes, origin, shape, whole_chunk, obj in geometry:
         if not bound or bound[0] != ck:
             loc = locations.get(ck)
             if loc is None:
@@ -709,10 +825,11 @@ def fetches_at(prefix: str, leaf_path: str, entry: dict, geometry: tuple[tuple, 
                 key = f"{prefix}/process_{loc['p']}/" + chunk_object_key(leaf_path, coords)
                 bound = (ck, key, 0, "get", True)
         _, key, base, op, whole = bound
+        checked = obj if whole else -1  # per-leaf objects: the size a whole read expects
         if whole_chunk:
-            out.append(Fetch(key, op, base, nbytes, origin, shape, whole))
+            out.append(Fetch(key, op, base, nbytes, origin, shape, whole, checked))
         else:
-            out.append(Fetch(key, "get_range", base + rel, nbytes, origin, shape, False))
+            out.append(Fetch(key, "get_range", base + rel, nbytes, origin, shape, False, checked))
     return out
 
 
@@ -787,6 +904,49 @@ class FetchItem:
     cast_flags: int = 0   # device address of the leaf's check word on the reader GPU
 
 
+MAX_PIECE_BYTES = 256 << 20
+
+
+def staging_budget(cfg, concurrent: int = 1) -> int:
+    """Largest fetch that may go through device staging: a quarter of the engine's
+    staging buffer (several items in flight), at most MAX_PIECE_BYTES."""
+    staging = cfg.sizing(concurrent)[2]
+    return max(1, min(MAX_PIECE_BYTES, staging // 4))
+
+
+def _direct_consumer(it: FetchItem) -> tuple[Destination | None, int]:
+    """The consumer on the reader GPU the fetched bytes land in as one contiguous run
+    without conversion (a direct H2D target), and the landing address."""
+    f = it.fetch
+    fetched = tuple(zip(f.origin, f.shape))
+    for d in it.consumers:
+        if d.gpu != it.reader_gpu or d.src_code:
+            continue
+        if not all(do <= fo and fo + fe <= do + de for (fo, fe), (do, de) in zip(fetched, d.ranges)):
+            continue
+        dshape = tuple(e for _, e in d.ranges)
+        doff = tuple(fo - do for (fo, _), (do, _) in zip(fetched, d.ranges))
+        if box_is_contiguous(dshape, doff, f.shape):
+            return d, d.address + box_flat_offset(dshape, doff) * d.itemsize
+    return None, 0
+
+
+def _within_staging(items: list[FetchItem], budget: int) -> list[FetchItem]:
+    """Items that need device staging (no direct consumer) and exceed ``budget`` become
+    several items over consecutive slabs of the fetch (still one read of each byte);
+    slabs no consumer meets are not read."""
+    out: list[FetchItem] = []
+    for it in items:
+        if it.fetch.nbytes <= budget or _direct_consumer(it)[0] is not None:
+            out.append(it)
+            continue
+        for f in split_fetch(it.fetch, budget):
+            box = tuple(zip(f.origin, f.shape))
+            if any(_intersect(box, d.ranges) is not None for d in it.consumers):
+                out.append(FetchItem(f, it.reader_gpu, it.consumers, it.cast_flags))
+    return out
+
+
 def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurrent: int = 1):
     """Fetch every item once onto its reader GPU and scatter it into every consumer
     (local or peer GPUs).  Admission / recording of the get ops as in execute_writes."""
@@ -794,6 +954,8 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
 
     if not items:
         return None
+    cfg = engine_cfg or native.EngineConfig()
+    items = _within_staging(items, staging_budget(cfg, concurrent))
     backend = store.backend
     keys = [it.fetch.key for it in items]
     store.sched_point()
@@ -826,9 +988,9 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
             inputs[i]["size"] = arr.size
     for it in items:
         size = int(inputs[input_index[it.fetch.key]]["size"])
-        if it.fetch.whole_file and size != it.fetch.nbytes:  # a per-leaf chunk object
+        if it.fetch.object_bytes >= 0 and size != it.fetch.object_bytes:  # a per-leaf chunk object
             raise CorruptionError(
-                f"chunk object {it.fetch.key!r} has {size} bytes, expected {it.fetch.nbytes}"
+                f"chunk object {it.fetch.key!r} has {size} bytes, expected {it.fetch.object_bytes}"
             )
         if it.fetch.file_off + it.fetch.nbytes > size:  # a span of an aggregated data file
             from .errors import BackendError
@@ -846,18 +1008,7 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     for j, it in enumerate(items):
         f = it.fetch
         fetched = tuple(zip(f.origin, f.shape))
-        direct = None
-        for d in it.consumers:
-            if d.gpu != it.reader_gpu or d.src_code:
-                continue
-            if not all(do <= fo and fo + fe <= do + de for (fo, fe), (do, de) in zip(fetched, d.ranges)):
-                continue
-            dshape = tuple(e for _, e in d.ranges)
-            doff = tuple(fo - do for (fo, _), (do, _) in zip(fetched, d.ranges))
-            if box_is_contiguous(dshape, doff, f.shape):
-                direct = d
-                direct_dst[j] = d.address + box_flat_offset(dshape, doff) * d.itemsize
-                break
+        direct, direct_dst[j] = _direct_consumer(it)
         first_copy[j] = len(cols["ext"])
         for d in it.consumers:
             if d is direct:
@@ -888,7 +1039,6 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     ritems["n_copies"] = n_copies
     copies = native.copy_table(cols["sb"], cols["ss"], cols["so"], cols["db"], cols["ds"], cols["do"],
                                cols["ext"], cols["isz"], cols["sdt"], cols["ddt"], cols["flg"])
-    cfg = engine_cfg or native.EngineConfig()
     with native.engine_lease(cfg, concurrent) as eng:
         stats = eng.load(ritems, inputs, copies)
     native.account_peer(peer_bytes)
