@@ -273,6 +273,36 @@ def _flatten_shardings(per_tree):
     return out
 
 
+METRIC = "checkpoint save+restore throughput (GB/s of tree bytes, save and restore each count once)"
+
+
+def bench_config(args, N: int) -> dict:
+    """The ``config`` object of BOTH arms' JSON lines: what workload the line measures
+    (tree, mesh, save mode, storage target) and nothing about how an arm runs it, so the
+    two lines of one configuration compare equal."""
+    if args.config == "c1":
+        workload = "C1 4 x (4096,4096) f32 unsharded (268435456 bytes), process 0 writes"
+        tree_bytes, layers = 4 * 4096 * 4096 * 4, 0
+    else:
+        leaves = llama_leaves(**dict(LLAMA3_8B, layers=args.layers))
+        tree_bytes, layers = sum(nbytes(s, dt) for _, _, s, dt in leaves), args.layers
+        mesh = {"c2": f"FSDP-{N} on dim 0", "c3": f"2x{N // 2} (replica x fsdp) mesh, replica-parallel save",
+                "c3ss": f"2x{N // 2} (replica x fsdp) mesh, single-slice save",
+                "c4": f"saved 1x{N} (FSDP-{N}) -> restored onto 2x{(args.restore_gpus or N) // 2} "
+                      f"(replica x fsdp)"}.get(args.config, args.config)
+        workload = (f"{args.config.upper()} Llama-3-8B bf16 params + fp32 Adam mu/nu, {len(leaves)} leaves, "
+                    f"{tree_bytes} bytes, {mesh}")
+    return {
+        "workload": workload + f"; {args.save_mode} save -> restore per step, {args.layout} layout",
+        "config": args.config,
+        "layers": layers,
+        "tree_bytes": tree_bytes,
+        "storage": "tmpfs huge=always" if args.storage == "hugetmpfs" else "tmpfs /dev/shm",
+        "parallelism": f"{N} GPU(s), one logical process per GPU",
+        "l2": "inputs (tree bytes) far larger than the 126 MB L2; no flush needed",
+    }
+
+
 class Workload:
     """One benchmark configuration (BASELINE.json configs)."""
 
@@ -450,6 +480,7 @@ def run_ours(args) -> dict:
         acc["launches"] += k["launches"]
 
     verified = {}
+    step_snap: list[float] = []
 
     def step(i: int, opts=None, verify: bool = False):
         """One save (call -> committed) + one restore (call -> every shard resident).
@@ -471,7 +502,9 @@ def run_ours(args) -> dict:
         ev1.record()
         t1 = time.perf_counter()
         if timing:
-            _add(ksave, native.kernel_timing_collect())
+            ks = native.kernel_timing_collect()
+            _add(ksave, ks)
+            step_snap.append(ks["ms_max"])  # this step's device snapshot (async mode)
         if abstract is None:
             out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=wl.save_mesh)
         else:
@@ -572,13 +605,15 @@ def run_ours(args) -> dict:
     before = native.totals()
     native.kernel_timing(True)
     timing = True
-    saves, restores, walls, blocks = [], [], [], []
+    saves, restores, walls, blocks, host_blocks, snaps = [], [], [], [], [], []
     for i in range(args.steps):
         s_ms, r_ms, ws, wr, b_ms = step(args.warmup + i)
         saves.append(d.max(s_ms))
         restores.append(d.max(r_ms))
         walls.append(d.max(ws + wr))
-        blocks.append(d.max(b_ms))
+        host_blocks.append(d.max(b_ms))
+        snaps.append(d.max(step_snap[-1]) if args.save_mode == "async" and step_snap else 0.0)
+        blocks.append(host_blocks[-1] + snaps[-1])
     native.kernel_timing(False)
     timing = False
     native.kernel_timing_collect()
@@ -626,11 +661,11 @@ def run_ours(args) -> dict:
     save_gbs = tree_bytes / (save_ms / 1e3) / 1e9
     restore_gbs = tree_bytes / (restore_ms / 1e3) / 1e9
 
-    snap_dev_ms = d.max(ksave["ms_max"]) if args.save_mode == "async" else 0.0
+    snap_dev_ms = statistics.mean(snaps) if args.save_mode == "async" else 0.0
     # async-save blocking vs the synchronous save it replaces: the timed steps give one
     # side, one extra save (untimed for `value`) in the other mode gives the other
     if args.save_mode == "async":
-        blocking_ms = statistics.mean(blocks)
+        blocking_ms = statistics.mean(host_blocks)
         other = step(args.warmup + args.steps, sync_opts, verify=True)
         sync_save_ms = d.max(other[0])
         async_total_ms = save_ms
@@ -644,11 +679,21 @@ def run_ours(args) -> dict:
         shutil.rmtree(os.path.join(base, "bench"), ignore_errors=True)
 
     kern = kernel_roofline(tv, native, state, rt, d, ksave, kload, args, step_ms, peer_gb)
+    reshard = (reshard_leg(tv, native, d, rt, wl, state, shardings, args, N, base)
+               if args.reshard_steps > 0 and wl.name == "c2" else None)
     e2e = end_to_end(tv, rt, wl, args, d, base) if not args.no_e2e else None
+    c5 = None
+    if args.c5_layers > 0 and wl.name == "c2":
+        # BASELINE configs[4] in the default line: the training loop's blocking time with a
+        # Checkpointer saving every step (its own smaller tree: keep_last=3 + 1 in flight
+        # must fit the RAM-backed storage next to nothing else)
+        del state
+        torch.cuda.empty_cache()
+        c5 = c5_loop(tv, d, rt, N, base, args.c5_layers, args.c5_steps, args.train_ms)
 
     peaks = measured_peaks()
     result = {
-        "metric": "checkpoint save+restore throughput (GB/s of tree bytes, save and restore each count once)",
+        "metric": METRIC,
         "value": round(value, 3),
         "unit": "GB/s",
         "n_gpus": N,
@@ -661,15 +706,12 @@ def run_ours(args) -> dict:
         "dtype": "u8",
         "payload_dtypes": "bf16 params + f32 Adam mu/nu, moved as bytes (no arithmetic on the path)",
         "data": "synthetic (random values generated on device, Llama-3-8B shapes)",
-        "config": {
-            "workload": wl.describe + f", {len(wl.leaves)} leaves, {tree_bytes} bytes",
-            "config": wl.name,
-            "layers": args.layers,
-            "tree_bytes": tree_bytes,
-            "storage": f"FilesystemBackend on {base} ({'tmpfs huge=always' if args.storage == 'hugetmpfs' else 'tmpfs /dev/shm'})",
-            "parallelism": f"{N} GPUs, one logical process per GPU" + (" (torchrun)" if d.on else " (threads runtime)"),
-            "l2": "inputs (tree bytes) far larger than the 126 MB L2; no flush needed",
-            "timing": "CUDA events on the current stream around save and restore, barrier+sync both sides, max over ranks",
+        "config": bench_config(args, N),
+        "arm": {
+            "storage_path": base,
+            "runtime": "torchrun (DistributedRuntime)" if d.on else "threads (SimulatedRuntime)",
+            "timing": "CUDA events on the current stream around save and restore, barrier+sync both sides, "
+                      "max over ranks",
         },
         "save_GBps": round(save_gbs, 3),
         "restore_GBps": round(restore_gbs, 3),
@@ -682,15 +724,23 @@ def run_ours(args) -> dict:
             "host_ms": round(blocking_ms, 2),
             "device_snapshot_ms": round(snap_dev_ms, 2),
             "note": "save() returns once the snapshot is enqueued on the caller's stream (host_ms); "
-                    "the snapshot kernel then holds that stream for device_snapshot_ms (longest "
-                    "launch in the timed steps) — both are counted as blocking",
+                    "the snapshot kernel then holds that stream for device_snapshot_ms (mean over the "
+                    "timed steps) — both are counted as blocking",
         },
         "async_total_ms": round(async_total_ms, 2),
         "sync_save_ms": round(sync_save_ms, 2),
         "async_blocking_frac_of_sync_save": round((blocking_ms + snap_dev_ms) / sync_save_ms, 4),
+        "async_blocking_ms_per_step": ({"p50": round(_pct(blocks, 50), 2), "p99": round(_pct(blocks, 99), 2),
+                                        "max": round(max(blocks), 2),
+                                        "p99_frac_of_sync_save": round(_pct(blocks, 99) / sync_save_ms, 4),
+                                        "how": "per timed step: host time in save_checkpoint + that step's "
+                                               "snapshot kernel (max over ranks)"}
+                                       if args.save_mode == "async" else None),
         "io_roofline": None,
         "roofline": kern,
         "e2e": e2e,
+        "c5": c5,
+        "reshard": reshard,
         "gpu_launches": int(kernels),
         "gpu_launches_breakdown": {
             "box_copy_kernel": int(kernels),
@@ -744,7 +794,7 @@ def run_ours(args) -> dict:
         }
         result["roofline"]["peak_source"] = peaks["source"]
         if not args.no_cpu_baseline and N == 1:  # rank 0 at N=1 only (the contract)
-            result["cpu_baseline"] = cpu_baseline(args, sample_layers=args.cpu_layers, root_dir=base)
+            result["cpu_baseline"] = cpu_baseline(args, root_dir=base)
     return result
 
 
@@ -769,26 +819,22 @@ def _storage_room(path: str):
         return None
 
 
-def run_c5(args) -> dict:
-    """C5: Checkpointer async save every step (keep_last=3) inside a synthetic training
-    loop; reports the time the training loop is blocked in save_step."""
+def _pct(xs, q):
+    """Nearest-rank percentile."""
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, max(0, math.ceil(q / 100 * len(xs)) - 1))]
+
+
+def c5_loop(tv, d, rt, N: int, base: str, layers: int, steps: int, train_ms: float,
+            inline_gc: bool = False) -> dict:
+    """C5 (BASELINE configs[4]): ``Checkpointer(keep_last=3)`` async save EVERY step of a
+    synthetic training loop (fixed GPU time + an in-place update of every param shard);
+    the blocking time is what the loop spends in ``save_step`` plus the snapshot
+    kernel's device time on the training stream (``training_manager.py:191-224``)."""
     import torch
 
-    import paper_2605_23066_b200 as tv
-
-    d = Dist()
-    d.init()
-    N = d.world if d.on else args.gpus
-    torch.cuda.set_device(d.local)
-    base = args.dir
-    if d.rank == 0:
-        shutil.rmtree(base, ignore_errors=True)
-        os.makedirs(base, exist_ok=True)
-    d.barrier()
-    backend = tv.FilesystemBackend(base)
     mesh = tv.Mesh.create([("fsdp", N)], process_count=N)
-    rt = open_runtime(tv, d, N, backend, gpus=list(range(N)))
-    leaves = llama_leaves(**dict(LLAMA3_8B, layers=args.layers))
+    leaves = llama_leaves(**dict(LLAMA3_8B, layers=layers))
     tree_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
     # keep_last=3 plus the save in flight live on the storage at once; on a RAM-backed
     # target that must fit host memory, or the kernel OOM-kills the job mid-save
@@ -804,23 +850,25 @@ def run_c5(args) -> dict:
     for i in range(2):
         d.barrier()
         t0 = time.perf_counter()
-        tv.save_checkpoint(rt, f"sync/{i}", state, shardings, tv.SaveOptions(sync=True)).wait()
+        tv.save_checkpoint(rt, f"c5sync/{i}", state, shardings, tv.SaveOptions(sync=True)).wait()
         sync_ms.append(d.max((time.perf_counter() - t0) * 1e3))
         d.barrier()
         if d.rank == 0:
-            shutil.rmtree(os.path.join(base, "sync"), ignore_errors=True)
+            shutil.rmtree(os.path.join(base, "c5sync"), ignore_errors=True)
     sync_save_ms = sync_ms[-1]
-    cycles = int(args.train_ms * 1.965e6)
-    ck = tv.Checkpointer(rt, "run", tv.RetentionPolicy(keep_last=3), tv.SaveOptions(sync=False),
-                         background_delete=not args.inline_gc)
-    blocking, waits, joins, gcs, bg = [], [], [], [], []
+    cycles = int(train_ms * 1.965e6)
+    ck = tv.Checkpointer(rt, "c5run", tv.RetentionPolicy(keep_last=3), tv.SaveOptions(sync=False),
+                         background_delete=not inline_gc)
+    blocking, waits, joins, gcs, bg, snap_dev = [], [], [], [], [], []
     phase_sums: dict[str, float] = {}
     from paper_2605_23066_b200 import native
+    from paper_2605_23066_b200 import timeline as _tlm
 
     native.kernel_timing_collect()
-    native.kernel_timing(True)  # the snapshot kernels' device time, collected after the loop
+    native.kernel_timing(True)  # the snapshot kernel's device time, per step
     t_start = time.perf_counter()
-    for step in range(args.steps):
+    prev = None
+    for step in range(steps):
         # synthetic training step: fixed GPU time + an in-place update of every param shard
         torch.cuda._sleep(cycles)
         for t in params:
@@ -830,12 +878,13 @@ def run_c5(args) -> dict:
         t0 = time.perf_counter()
         handle = ck.save_step(step, state, shardings)
         blocking.append(d.max((time.perf_counter() - t0) * 1e3))
+        torch.cuda.synchronize()  # the snapshot kernel queued on the training stream
+        kt = native.kernel_timing_collect()
+        snap_dev.append(d.max(kt["ms_max"]))
         waits.append(d.max(ck.last_wait_seconds * 1e3))
         joins.append(d.max(ck.last_join_seconds * 1e3))
         gcs.append(d.max(ck.last_gc_seconds * 1e3))
-        if step > 0:  # the previous save has been joined: its per-phase timeline is final
-            from paper_2605_23066_b200 import timeline as _tlm
-
+        if prev is not None:  # the previous save has been joined: its per-phase timeline is final
             for k, v in _tlm.LAST_SAVE.get(d.rank if d.on else 0, {}).items():
                 phase_sums[k] = phase_sums.get(k, 0.0) + v
             tl = prev.handles[0].session.timeline
@@ -844,47 +893,79 @@ def run_c5(args) -> dict:
         prev = handle
     ck.close()
     native.kernel_timing(False)
-    kt = native.kernel_timing_collect()
-    snap_dev_ms = d.max(kt["ms_total"] / max(1, kt["launches"]))
+    native.kernel_timing_collect()
     loop_s = time.perf_counter() - t_start
     kept = ck.all_steps()
-    assert kept == list(range(args.steps - 3, args.steps)), kept
+    assert kept == list(range(steps - 3, steps)), kept
     snap = [b - w for b, w in zip(blocking, waits)]
-    steady = blocking[1:] or blocking
-    result = {
-        "metric": "async-save blocking time per training step (Checkpointer.save_step every step)",
-        "value": round(statistics.mean(steady) + snap_dev_ms, 2),
-        "unit": "ms",
-        "higher_is_better": False,
-        "n_gpus": N,
-        "steps": args.steps,
-        "config": {
-            "workload": f"C5 Checkpointer(keep_last=3, async) every step over {args.steps} steps, "
-                        f"Llama-3-8B {args.layers} layers ({tree_bytes} bytes) FSDP-{N}, synthetic "
-                        f"training step = {args.train_ms} ms GPU time + in-place param update, "
-                        f"retention deletes {'inline (reference)' if args.inline_gc else 'in the background'}",
-            "config": "c5",
-        },
-        "blocking_ms_mean": round(statistics.mean(steady) + snap_dev_ms, 2),
-        "blocking_host_ms_mean": round(statistics.mean(steady), 2),
-        "snapshot_device_ms_mean": round(snap_dev_ms, 2),
-        "blocking_ms_p50": round(statistics.median(steady), 2),
+    total = [b + s for b, s in zip(blocking, snap_dev)]
+    steady = total[1:] or total  # the first save_step also warms plan caches
+    host_steady = blocking[1:] or blocking
+    mean = statistics.mean(steady)
+    del state, params
+    d.barrier()
+    if d.rank == 0:
+        shutil.rmtree(os.path.join(base, "c5run"), ignore_errors=True)
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"C5 Checkpointer(keep_last=3, async) every step over {steps} steps, Llama-3-8B "
+                    f"{layers} layers ({tree_bytes} bytes) FSDP-{N}, synthetic training step = {train_ms} ms "
+                    f"GPU time + in-place param update, retention deletes "
+                    f"{'inline (reference)' if inline_gc else 'in the background'}",
+        "tree_bytes": tree_bytes,
+        "blocking_ms_mean": round(mean, 2),
+        "blocking_ms_p50": round(_pct(steady, 50), 2),
+        "blocking_ms_p99": round(_pct(steady, 99), 2),
         "blocking_ms_max": round(max(steady), 2),
+        "blocking_host_ms_mean": round(statistics.mean(host_steady), 2),
+        "snapshot_device_ms_mean": round(statistics.mean(snap_dev[1:] or snap_dev), 2),
         "wait_on_previous_ms_mean": round(statistics.mean(waits[1:] or waits), 2),
         "own_sync_phase_ms_mean": round(statistics.mean(snap[1:] or snap), 2),
         "join_previous_ms_mean": round(statistics.mean(joins[1:] or joins), 2),
         "retention_gc_ms_mean": round(statistics.mean(gcs[1:] or gcs), 2),
         "background_save_ms_mean": round(statistics.mean(bg), 2) if bg else None,
         "sync_save_ms": round(sync_save_ms, 2),
-        "blocking_frac_of_sync_save": round((statistics.mean(steady) + snap_dev_ms) / sync_save_ms, 4),
+        "blocking_frac_of_sync_save": round(mean / sync_save_ms, 4),
+        "blocking_p99_frac_of_sync_save": round(_pct(steady, 99) / sync_save_ms, 4),
         "loop_seconds": round(loop_s, 2),
         "retained_steps": kept,
-        "save_phases_ms_mean_rank0": {k: round(v / max(1, args.steps - 1), 2) for k, v in phase_sums.items()},
+        "save_phases_ms_mean_rank0": {k: round(v / max(1, steps - 1), 2) for k, v in phase_sums.items()},
+        "how": "blocking per step = wall time in save_step (max over ranks) + the snapshot kernel's device "
+               "time on the training stream (CUDA events, libtvgpu tv_kernel_timing); first step excluded",
     }
+
+
+def run_c5(args) -> dict:
+    """C5 as the whole bench line (``--config c5``)."""
+    import torch
+
+    import paper_2605_23066_b200 as tv
+
+    d = Dist()
+    d.init()
+    N = d.world if d.on else args.gpus
+    torch.cuda.set_device(d.local)
+    base = args.dir
+    if d.rank == 0:
+        shutil.rmtree(base, ignore_errors=True)
+        os.makedirs(base, exist_ok=True)
+    d.barrier()
+    backend = tv.FilesystemBackend(base)
+    rt = open_runtime(tv, d, N, backend, gpus=list(range(N)))
+    res = c5_loop(tv, d, rt, N, base, args.layers, args.steps, args.train_ms, args.inline_gc)
     d.barrier()
     if d.rank == 0:
         shutil.rmtree(base, ignore_errors=True)
-    return result
+    return {
+        "metric": "async-save blocking time per training step (Checkpointer.save_step every step)",
+        "value": res["blocking_ms_mean"],
+        "unit": "ms",
+        "higher_is_better": False,
+        "n_gpus": N,
+        "steps": args.steps,
+        "config": {"workload": res["workload"], "config": "c5"},
+        **{k: v for k, v in res.items() if k != "workload"},
+    }
 
 
 def time_launch(fn, gpu: int, reps: int = 5, warmup: int = 3) -> tuple[float, float]:
@@ -1030,6 +1111,68 @@ def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, st
     }
 
 
+def reshard_leg(tv, native, d, rt, wl, state, shardings, args, N: int, base: str) -> dict:
+    """BASELINE's reshard GB/s in the default line: the step's checkpoint (FSDP-N) restored
+    onto another sharding of the same GPUs — at N >= 2 the C4 target shape (replica 2 x
+    fsdp N/2: every stored chunk is consumed by two GPUs, read once, fanned out over
+    NVLink by the unpack kernel); at N = 1 a column split (None, "tp") over 2 logical
+    devices (every byte through the unpack kernel).  Timed like the step (CUDA events,
+    barrier + sync, max over ranks); the last restore is verified on the device."""
+    import torch
+
+    if N >= 2:
+        mesh = tv.Mesh.create([("replica", 2), ("fsdp", N // 2)], process_count=N, replica_axis="replica")
+        spec_fn, target = fsdp_spec, f"2x{N // 2} (replica x fsdp), {N} processes"
+        rrt = rt
+    else:
+        mesh = tv.Mesh.create([("tp", 2)], process_count=2)
+        spec_fn = lambda s: (None, "tp") if len(s) == 2 else ("tp",)  # noqa: E731
+        target, rrt = "(None, 'tp') column split over 2 logical devices on GPU 0", \
+            tv.SimulatedRuntime(2, rt.backend, gpus=[0])
+    tree: dict = {}
+    for t, path, shape, dtype in wl.leaves:
+        node = tree.setdefault(t, {})
+        parts = path.split("/")
+        for p in parts[:-1]:
+            node = node.setdefault(p, {})
+        node[parts[-1]] = tv.AbstractLeaf("array", shape, dtype,
+                                          tv.Sharding(mesh, tv.PartitionSpec(spec_fn(shape)), shape))
+    abstract = {"state": tree}
+    path = "bench/reshard"
+    tv.save_checkpoint(rt, path, state, shardings, tv.SaveOptions(sync=True)).wait()
+    times, nv = [], []
+    verified = {}
+    for i in range(args.reshard_steps):
+        before = native.totals()["peer_bytes"]
+        d.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = tv.load_checkpoint(rrt, path, abstract, tv.LoadOptions())
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(d.max(e0.elapsed_time(e1)))
+        nv.append(d.sum(native.totals()["peer_bytes"] - before))
+        if i == args.reshard_steps - 1:
+            nb, bad = verify_restore(tv, state, out)
+            verified = {"bytes_compared": int(d.sum(nb)), "mismatched_boxes": int(d.sum(bad))}
+        del out
+        torch.cuda.empty_cache()
+    d.barrier()
+    if d.rank == 0:
+        shutil.rmtree(os.path.join(base, "bench"), ignore_errors=True)
+    ms = statistics.mean(times)
+    return {
+        "target": target,
+        "GBps": round(wl.tree_bytes / (ms / 1e3) / 1e9, 3),
+        "ms": round(ms, 2),
+        "restores": args.reshard_steps,
+        "nvlink_GB_per_restore": round(statistics.mean(nv) / 1e9, 3),
+        "restore_verified": dict(verified, how="every restored shard's overlap with every saved shard, "
+                                               "torch.equal on the device (all ranks)"),
+    }
+
+
 def verify_restore(tv, state, out) -> tuple[int, int]:
     """Restored shards vs the saved state, byte for byte on the device: each target shard's
     overlap with each addressable source shard must be equal (any target sharding).
@@ -1073,17 +1216,18 @@ def _device_tensors(leaf):
 
 
 def end_to_end(tv, rt, wl, args, d, base) -> dict:
-    """Same metric through the host-array API: inputs H2D from pinned host memory and the
-    restored shards D2H into pinned host memory, inside the timed region.  Runs on a
-    reduced-depth tree when host RAM cannot hold inputs + outputs + the checkpoint."""
+    """Same metric through the public API with HOST buffers, on the same bounded sample
+    the reference arm times (``sample_leaves``): per step the inputs go H2D from pinned
+    host memory, then ``save_checkpoint`` (the step's save mode) + ``wait()`` +
+    ``load_checkpoint``, then the restored shards go D2H into pinned host memory — all
+    inside the timed region.  Mesh: our arm's (one logical process per GPU)."""
+    import dataclasses
+
     import torch
 
     mesh = wl.save_mesh
-    if wl.name == "c1":
-        layers, e_leaves = 0, wl.leaves
-    else:
-        layers = args.e2e_layers
-        e_leaves = llama_leaves(**dict(LLAMA3_8B, layers=layers))
+    e_leaves = sample_leaves(wl.name, args.cpu_layers)
+    opts = dataclasses.replace(wl.save_options, sync=args.save_mode == "sync")
     # host copies of this process's shards (pinned), generated from the device state
     state, shardings = build_state(tv, rt, mesh, e_leaves, seed=7, spec_fn=wl.spec_fn)
     host = {}
@@ -1108,7 +1252,7 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
                     t.copy_(host[(path, dev)], non_blocking=True)
         torch.cuda.synchronize()
         path = f"e2e/step_{i}"
-        tv.save_checkpoint(rt, path, state, shardings, wl.save_options).wait()
+        tv.save_checkpoint(rt, path, state, shardings, opts).wait()
         out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=mesh)
         for tree in out.values():  # D2H: restored shards to pinned host memory
             for p, leaf in tv.flatten(tree):
@@ -1132,42 +1276,43 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
         "h2d_bytes_per_step": int(total_local),
         "d2h_bytes_per_step": int(total_local),
         "tree_bytes": tree_bytes,
-        "layers": layers,
+        "sample": (f"the reference arm's sample: {len(e_leaves)} leaves"
+                   + ("" if wl.name == "c1" else f" ({args.cpu_layers} layers + final_norm, no embed/lm_head)")),
         "config": wl.name,
-        "api": "save_checkpoint(sync) + load_checkpoint with H2D of inputs / D2H of results (pinned)",
+        "api": f"save_checkpoint({args.save_mode}) + wait() + load_checkpoint, with H2D of the inputs and "
+               "D2H of the restored shards (pinned) inside the timed region",
         "steps": args.e2e_steps,
     }
 
 
-# -- CPU baseline: the oracle port of the reference ------------------------------------------------
+# -- the reference arm / CPU baseline -----------------------------------------------------------
 
 
-def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_dir: str | None = None,
-                 steps: int = 1, warmup: int = 0) -> dict:
-    """The reference's save + restore (oracle/treevault_oracle.py restating
-    save_pipeline/chunkstore/load_pipeline) on a bounded sample of the workload, one host
-    thread per simulated process, same directory type as the GPU run."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+def sample_leaves(config: str, layers: int):
+    """The bounded sample both CPU legs and our e2e run: the whole C1 tree for c1; else
+    ``layers`` transformer layers of the C2 tree plus final_norm (no embed / lm_head)."""
+    if config == "c1":
+        return [("model", f"a{i}", (4096, 4096), "f32") for i in range(4)]
+    return [(t, p, s, dt) for t, p, s, dt in llama_leaves(**dict(LLAMA3_8B, layers=layers))
+            if not p.startswith(("embed", "lm_head"))]
+
+
+def reference_processes(config: str) -> int:
+    """Simulated processes of the reference's multi-controller mode (one host thread
+    each): every host thread it can use (a power of two), 1 for C1 (unsharded)."""
+    if config == "c1":
+        return 1
+    cores = len(os.sched_getaffinity(0))
+    return max(1, min(64, 1 << (cores.bit_length() - 1)))
+
+
+def _host_tree(leaves, seed=0):
     import numpy as np
 
-    import treevault_oracle as orc
-
-    cores = len(os.sched_getaffinity(0))
-    P = processes or max(1, min(64, 1 << (cores.bit_length() - 1)))  # all host threads (power of 2)
-    c1 = getattr(args, "config", "c2") == "c1"
-    if c1:  # BASELINE configs[0] itself: 4 x (4096, 4096) f32, unsharded, one process
-        P = 1
-        leaves = [("model", f"a{i}", (4096, 4096), "f32") for i in range(4)]
-    else:
-        dims = dict(LLAMA3_8B)
-        dims["layers"] = sample_layers
-        leaves = [(t, p, s, dt) for t, p, s, dt in llama_leaves(**dims)
-                  if not p.startswith(("embed", "lm_head"))]
-    rng = np.random.default_rng(0)
-    tree: dict = {"state": {}}
-    specs: dict = {"state": {}}
+    rng = np.random.default_rng(seed)
+    tree: dict = {}
     for t, p, shape, dt in leaves:
-        node = tree["state"].setdefault(t, {})
+        node = tree.setdefault(t, {})
         parts = p.split("/")
         for q in parts[:-1]:
             node = node.setdefault(q, {})
@@ -1175,11 +1320,92 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
             data = rng.integers(0, 1 << 16, size=shape, dtype=np.uint16)
         else:
             data = rng.standard_normal(size=shape, dtype=np.float32)
-        node[parts[-1]] = ("array", dt, data)
-        if not c1:
+        node[parts[-1]] = data
+    return tree
+
+
+def reference_leg(args, root_dir: str, steps: int, warmup: int) -> dict:
+    """The UNMODIFIED reference (oracle/_ref, staged by oracle/ref_recipe.py from
+    /root/reference/pkg/src/treevault) through its own public API: per step an async
+    ``save_checkpoint(...).wait()`` (``save_pipeline.py:594-622``) and a
+    ``load_checkpoint`` of it (``load_pipeline.py:538-580``) on the same storage target as
+    our arm, P simulated processes (one host thread each), FSDP-P on dim 0."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref_recipe
+
+    rv = ref_recipe.load_reference()
+    config = getattr(args, "config", "c2")
+    leaves = sample_leaves(config, args.cpu_layers)
+    P = reference_processes(config)
+    host = _host_tree(leaves)
+    mesh = rv.Mesh.create([("fsdp", P)], process_count=P)
+    tree, shardings = {}, {}
+    for t, p, shape, dt in leaves:
+        node, src = tree.setdefault(t, {}), host[t]
+        parts = p.split("/")
+        for q in parts[:-1]:
+            node, src = node.setdefault(q, {}), src[q]
+        node[parts[-1]] = rv.DenseArray(dt, src[parts[-1]])
+        if config != "c1":
+            shardings[f"{t}/{p}"] = rv.Sharding(mesh, rv.PartitionSpec(("fsdp",) + (None,) * (len(shape) - 1)), shape)
+    sample_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
+    root = os.path.join(root_dir, "reference_arm")
+    saves, restores = [], []
+    for i in range(warmup + steps):
+        shutil.rmtree(root, ignore_errors=True)
+        os.makedirs(root)
+        rt = rv.SimulatedRuntime(P, rv.FilesystemBackend(root))
+        t0 = time.perf_counter()
+        rv.save_checkpoint(rt, "ck", {"state": tree}, {"state": shardings} if shardings else None,
+                           rv.SaveOptions(sync=False)).wait()
+        t1 = time.perf_counter()
+        out = rv.load_checkpoint(rt, "ck", None, rv.LoadOptions(), current_mesh=mesh if shardings else None)
+        t2 = time.perf_counter()
+        del out
+        if i >= warmup:
+            saves.append(t1 - t0)
+            restores.append(t2 - t1)
+    shutil.rmtree(root, ignore_errors=True)
+    t_save, t_restore = statistics.mean(saves), statistics.mean(restores)
+    return {
+        "value": round(2 * sample_bytes / (t_save + t_restore) / 1e9, 3),
+        "unit": "GB/s",
+        "cores": P,
+        "kind": "reference",
+        "sample": (f"the whole C1 tree (4 x (4096,4096) f32, unsharded, one process), {sample_bytes} bytes"
+                   if config == "c1" else
+                   f"{args.cpu_layers} transformer layers of the C2 tree + final_norm (no embed/lm_head), "
+                   f"{sample_bytes} bytes, FSDP-{P} over {P} simulated processes (one host thread each)")
+                  + f"; async save().wait() + load_checkpoint per step, mean of {steps} after {warmup} warm-up",
+        "sample_bytes": sample_bytes,
+        "save_GBps": round(sample_bytes / t_save / 1e9, 3),
+        "restore_GBps": round(sample_bytes / t_restore / 1e9, 3),
+        "implementation": "treevault (unmodified, oracle/_ref) via save_checkpoint / load_checkpoint",
+    }
+
+
+def port_leg(args, root_dir: str, steps: int = 1, warmup: int = 0) -> dict:
+    """Cross-check: the oracle port (oracle/treevault_oracle.py restating save_pipeline /
+    chunkstore / load_pipeline) on the same sample and process count."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import treevault_oracle as orc
+
+    config = getattr(args, "config", "c2")
+    leaves = sample_leaves(config, args.cpu_layers)
+    P = reference_processes(config)
+    host = _host_tree(leaves)
+    tree: dict = {"state": {}}
+    specs: dict = {"state": {}}
+    for t, p, shape, dt in leaves:
+        node, src = tree["state"].setdefault(t, {}), host[t]
+        parts = p.split("/")
+        for q in parts[:-1]:
+            node, src = node.setdefault(q, {}), src[q]
+        node[parts[-1]] = ("array", dt, src[parts[-1]])
+        if config != "c1":
             specs["state"][f"{t}/{p}"] = ([("fsdp", P)], P, None, ("fsdp",) + (None,) * (len(shape) - 1))
     sample_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
-    root = os.path.join(root_dir or args.dir, "cpu_baseline")
+    root = os.path.join(root_dir, "port_leg")
     saves, restores = [], []
     for i in range(warmup + steps):
         shutil.rmtree(root, ignore_errors=True)
@@ -1204,50 +1430,51 @@ def cpu_baseline(args, sample_layers: int, processes: int | None = None, root_di
             restores.append(t_restore)
     shutil.rmtree(root, ignore_errors=True)
     t_save, t_restore = statistics.mean(saves), statistics.mean(restores)
-    value = 2 * sample_bytes / (t_save + t_restore) / 1e9
-    return {
-        "value": round(value, 3),
-        "unit": "GB/s",
-        "cores": P,
-        "kind": "port",
-        "sample": (f"the whole C1 tree (4 x (4096,4096) f32, unsharded, one process), {sample_bytes} bytes"
-                   if c1 else
-                   f"{sample_layers} transformer layers of the C2 tree (no embed/lm_head), "
-                   f"{sample_bytes} bytes, FSDP-{P} over {P} simulated processes (one host thread each)")
-                  + f", save + restore per step, mean of {steps} after {warmup} warm-up",
-        "save_GBps": round(sample_bytes / t_save / 1e9, 3),
-        "restore_GBps": round(sample_bytes / t_restore / 1e9, 3),
-    }
+    return {"value": round(2 * sample_bytes / (t_save + t_restore) / 1e9, 3), "unit": "GB/s", "cores": P,
+            "kind": "port", "sample_bytes": sample_bytes, "steps": steps, "warmup": warmup}
+
+
+def cpu_baseline(args, root_dir: str) -> dict:
+    """``cpu_baseline`` of our line (rank 0, N=1): the reference leg on a bounded sample
+    (one warm-up + one timed step), with the port beside it as a cross-check."""
+    res = reference_leg(args, root_dir, steps=1, warmup=1)
+    try:
+        res["port_cross_check"] = port_leg(args, root_dir)
+    except Exception as exc:  # noqa: BLE001 - a cross-check must not sink the bench line
+        res["port_cross_check"] = {"error": repr(exc)}
+    return res
 
 
 def run_reference(args) -> dict:
-    """The reference arm: the reference's CPU algorithm (the oracle port; the reference is
-    Python and cannot travel to the GPU box) on the box's host cores, --warmup W + --steps K
-    save+restore steps of a bounded sample of the same C2 workload, same storage target."""
+    """The reference arm: the unmodified reference on the box's host cores, --warmup W +
+    --steps K save+restore steps of a bounded sample of OUR arm's workload (same
+    ``config`` object, same storage target), rank 0 only."""
     d = Dist()
-    res = cpu_baseline(args, sample_layers=args.cpu_layers,
-                       root_dir=prepare_storage(args, d) if args.storage != "shm" else None,
-                       steps=args.steps, warmup=args.warmup)
+    base = prepare_storage(args, d)
+    os.makedirs(base, exist_ok=True)
+    res = reference_leg(args, base, steps=args.steps, warmup=args.warmup)
     N = d.world if d.on else args.gpus
     return {
         "impl": "reference",
-        "metric": "checkpoint save+restore throughput (GB/s of tree bytes, save and restore each count once)",
+        "metric": METRIC,
         "value": res["value"],
         "unit": "GB/s",
         "n_gpus": N,
         "steps": args.steps,
         "warmup": args.warmup,
         "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
         "dtype": "u8",
-        "payload_dtypes": "bf16 params + f32 Adam mu/nu, moved as bytes (no arithmetic on the path)",
+        "payload_dtypes": "bf16 params (as <u2 bit patterns: the reference has no bf16) + f32 Adam mu/nu, "
+                          "moved as bytes (no arithmetic on the path)",
         "data": "synthetic (numpy RNG, Llama-3-8B shapes)",
-        "config": {"workload": (f"C1: {res['sample']}" if args.config == "c1" else
-                                f"C2 Llama-3-8B bf16 params + fp32 Adam mu/nu (bounded sample: {res['sample']})"),
-                   "config": args.config, "storage": "oracle port on the same storage target as our arm"},
+        "config": bench_config(args, N),
         "save_GBps": res["save_GBps"],
         "restore_GBps": res["restore_GBps"],
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample", "implementation")},
+        "e2e": {"value": res["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "tree_bytes": res["sample_bytes"]},
     }
 
 
@@ -1258,8 +1485,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32)
-    ap.add_argument("--e2e-layers", type=int, default=8)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-layers", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dir", default="/dev/shm/tvbench")
@@ -1273,6 +1499,11 @@ def main() -> None:
                     help="async (default): each step's save is an async save + wait; sync: sync save")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--train-ms", type=float, default=1000.0)
+    ap.add_argument("--c5-layers", type=int, default=8,
+                    help="default line: Llama depth of the embedded C5 Checkpointer loop (0 = skip)")
+    ap.add_argument("--c5-steps", type=int, default=20)
+    ap.add_argument("--reshard-steps", type=int, default=3,
+                    help="default line: restores onto another sharding after the timed steps (0 = skip)")
     ap.add_argument("--inline-gc", action="store_true", help="c5: retention deletes inside wait() (reference)")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -807,7 +807,9 @@ class SaveRun {
       }
     }
     for (auto& d : s.d2h) {
-      if (cudaMemcpyAsync(host + d.slot_off, d.src, d.n, cudaMemcpyDeviceToHost, stream) !=
+      // cudaMemcpyDefault: the source is HBM, or pinned host memory when the async
+      // snapshot fell back to a host arena (save_pipeline._snapshot_arena); UVA resolves it.
+      if (cudaMemcpyAsync(host + d.slot_off, d.src, d.n, cudaMemcpyDefault, stream) !=
           cudaSuccess) {
         err_.set(TV_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(cudaGetLastError()));
         return false;

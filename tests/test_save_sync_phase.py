@@ -1,0 +1,57 @@
+"""Host logic of the save's synchronous phase (CPU): the cyclic GC is paused for the
+phase (nesting-safe across threads) and the caller's streams are captured on its own
+thread (empty without a GPU)."""
+
+from __future__ import annotations
+
+import gc
+import threading
+
+from paper_2605_23066_b200 import save_pipeline as sp
+
+
+def test_gc_paused_nests_and_restores():
+    assert gc.isenabled()
+    with sp._gc_paused():
+        assert not gc.isenabled()
+        with sp._gc_paused():
+            assert not gc.isenabled()
+        assert not gc.isenabled()
+    assert gc.isenabled()
+
+
+def test_gc_paused_across_threads():
+    inside = threading.Event()
+    release = threading.Event()
+
+    def other():
+        with sp._gc_paused():
+            inside.set()
+            release.wait(5)
+
+    t = threading.Thread(target=other)
+    t.start()
+    inside.wait(5)
+    with sp._gc_paused():
+        assert not gc.isenabled()
+    assert not gc.isenabled()  # the other thread's pause is still open
+    release.set()
+    t.join()
+    assert gc.isenabled()
+
+
+def test_gc_paused_keeps_a_disabled_collector_disabled():
+    gc.disable()
+    try:
+        with sp._gc_paused():
+            pass
+        assert not gc.isenabled()
+    finally:
+        gc.enable()
+
+
+def test_caller_streams_without_gpu():
+    class RT:
+        gpus = [0]
+
+    assert sp.caller_streams(RT()) == {}
