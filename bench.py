@@ -218,50 +218,50 @@ class Dist:
 # -- workload ------------------------------------------------------------------------------------
 
 
-def build_state(tv, rt, mesh, leaves, seed=0, spec_fn=None):
-    """Device shards of every leaf for the devices this process owns (synthetic values
-    generated on the GPU: N(0, 0.02) params, N(0, 1e-3) mu, N(0,1e-3)^2 nu)."""
+def gen_shard(i: int, tree: str, dtype: str, ranges, seed: int, gpu: int):
+    """The synthetic values of leaf ``i``'s box ``ranges`` (a shard), generated on ``gpu``:
+    N(0, 0.02) params, N(0, 1e-3) mu, N(0, 1e-3)^2 nu, seeded by the leaf and the box's
+    first row (replicas of a range hold identical values).  Deterministic, so any rank
+    can regenerate any shard to verify a restore against."""
     import torch
 
-    gen = torch.Generator(device="cuda")
+    with torch.cuda.device(gpu):
+        gen = torch.Generator(device=f"cuda:{gpu}")
+        gen.manual_seed(1000 * (i + 1) + (ranges[0][0] if ranges else 0) + seed)
+        ext = tuple(e for _, e in ranges)
+        t = torch.empty(ext, dtype=torch.float32 if dtype == "f32" else torch.bfloat16, device=f"cuda:{gpu}")
+        t.normal_(0.0, 0.02 if tree == "params" else 1e-3, generator=gen)
+        if tree == "nu":
+            t.mul_(t)
+    return t
+
+
+def build_state(tv, rt, mesh, leaves, seed=0, spec_fn=None):
+    """Device shards of every leaf for the devices this process owns (``gen_shard``)."""
+    import torch
+
     trees, shardings = {}, {}
     owned = set(rt.addressable_processes)
     for i, (tree, path, shape, dtype) in enumerate(leaves):
         spec = (spec_fn or (lambda s: ("fsdp",) + (None,) * (len(s) - 1)))(shape)
+        node = trees.setdefault(tree, {})
+        parts = path.split("/")
+        for p in parts[:-1]:
+            node = node.setdefault(p, {})
         if spec is None:  # unsharded leaf: one global array on process 0's GPU
             gpu = rt.gpu_of_process(0)
-            gen.manual_seed(1000 * (i + 1) + seed)
-            t = torch.empty(shape, dtype=torch.float32 if dtype == "f32" else torch.bfloat16, device=f"cuda:{gpu}")
-            t.normal_(0.0, 1.0, generator=gen)
-            node = trees.setdefault(tree, {})
-            parts = path.split("/")
-            for p in parts[:-1]:
-                node = node.setdefault(p, {})
-            node[parts[-1]] = tv.DenseArray(dtype, t)
+            node[parts[-1]] = tv.DenseArray(dtype, gen_shard(i, tree, dtype, tuple((0, e) for e in shape),
+                                                             seed, gpu))
             continue
         s = tv.Sharding(mesh, tv.PartitionSpec(spec), shape)
         shards = {}
         for sh in tv.shards_of(s):
             if mesh.process_of(sh.device) not in owned:
                 continue
-            gpu = rt.gpu_of_device(sh.device)
-            # replicas of a range hold identical values (seeded by the range, not the device)
-            gen.manual_seed(1000 * (i + 1) + sh.ranges[0][0] + seed)
-            ext = tuple(e for _, e in sh.ranges)
-            with torch.cuda.device(gpu):
-                t = torch.empty(ext, dtype=torch.float32 if dtype == "f32" else torch.bfloat16,
-                                device=f"cuda:{gpu}")
-                t.normal_(0.0, 0.02 if tree == "params" else 1e-3, generator=gen)
-                if tree == "nu":
-                    t.mul_(t)
-            shards[sh.device] = t
-        leaf = tv.ShardedArray(dtype, s, shards)
-        node = trees.setdefault(tree, {})
-        parts = path.split("/")
-        for p in parts[:-1]:
-            node = node.setdefault(p, {})
-        node[parts[-1]] = leaf
+            shards[sh.device] = gen_shard(i, tree, dtype, sh.ranges, seed, rt.gpu_of_device(sh.device))
+        node[parts[-1]] = tv.ShardedArray(dtype, s, shards)
         shardings.setdefault(tree, {})[path] = s
+    torch.cuda.synchronize()
     return {"state": trees}, {"state": _flatten_shardings(shardings)}
 
 
@@ -456,8 +456,13 @@ def run_ours(args) -> dict:
     rrt = rt
     if wl.restore_P is not None and wl.restore_P != P:
         if d.on:
-            raise SystemExit("a restore onto a different process count needs the threads runtime (no torchrun)")
-        rrt = tv.SimulatedRuntime(wl.restore_P, backend, gpus=list(range(min(N, wl.restore_P))))
+            # restore onto fewer ranks than saved (C4 "saved on 8, restored onto 4"): the
+            # first restore_P ranks form the restoring job; the others sit the restore out
+            if wl.restore_P > d.world:
+                raise SystemExit(f"--restore-gpus {wl.restore_P} > {d.world} ranks")
+            rrt = tv.DistributedRuntime.subgroup(backend, list(range(wl.restore_P)))
+        else:
+            rrt = tv.SimulatedRuntime(wl.restore_P, backend, gpus=list(range(min(N, wl.restore_P))))
     state, shardings = build_state(tv, rt, wl.save_mesh, wl.leaves, spec_fn=wl.spec_fn)
     abstract = wl.abstract() if wl.restore_mesh is not None else None
     torch.cuda.synchronize()
@@ -507,15 +512,17 @@ def run_ours(args) -> dict:
             step_snap.append(ks["ms_max"])  # this step's device snapshot (async mode)
         if abstract is None:
             out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=wl.save_mesh)
-        else:
+        elif rrt is not None:
             out = tv.load_checkpoint(rrt, path, abstract, tv.LoadOptions())
+        else:  # this rank is outside the restoring job
+            out = None
         ev2.record()
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         if timing:
             _add(kload, native.kernel_timing_collect())
         if verify:  # outside every timed number: restored bytes == saved state, on device
-            nb, bad = verify_restore(tv, state, out)
+            nb, bad = verify_restore(tv, state, out, wl.leaves) if out is not None else (0, 0)
             verified["bytes_compared"] = int(d.sum(nb))
             verified["mismatched_boxes"] = int(d.sum(bad))
         d.barrier()
@@ -1154,7 +1161,7 @@ def reshard_leg(tv, native, d, rt, wl, state, shardings, args, N: int, base: str
         times.append(d.max(e0.elapsed_time(e1)))
         nv.append(d.sum(native.totals()["peer_bytes"] - before))
         if i == args.reshard_steps - 1:
-            nb, bad = verify_restore(tv, state, out)
+            nb, bad = verify_restore(tv, state, out, wl.leaves)
             verified = {"bytes_compared": int(d.sum(nb)), "mismatched_boxes": int(d.sum(bad))}
         del out
         torch.cuda.empty_cache()
@@ -1173,12 +1180,16 @@ def reshard_leg(tv, native, d, rt, wl, state, shardings, args, N: int, base: str
     }
 
 
-def verify_restore(tv, state, out) -> tuple[int, int]:
+def verify_restore(tv, state, out, leaves=None, seed: int = 0) -> tuple[int, int]:
     """Restored shards vs the saved state, byte for byte on the device: each target shard's
-    overlap with each addressable source shard must be equal (any target sharding).
+    overlap with EVERY source shard must be equal (any target sharding).  Source shards
+    this process does not hold (torchrun: other ranks' shards) are regenerated on the
+    target's GPU with ``gen_shard`` when ``leaves`` (the workload's leaf list) is given.
     Returns (bytes compared, mismatching boxes)."""
     import torch
 
+    index = {f"{t}/{p}": (i, t, dt) for i, (t, p, _, dt) in enumerate(leaves)} if leaves else {}
+    ints = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
     compared = bad = 0
     for name, tree in out.items():
         src = dict(tv.flatten(state[name]))
@@ -1186,11 +1197,14 @@ def verify_restore(tv, state, out) -> tuple[int, int]:
             ref = src[path]
             if not hasattr(leaf, "shards") or not hasattr(ref, "shards"):
                 continue
-            s_ranges, t_ranges = ref.shard_ranges(), leaf.shard_ranges()
+            t_ranges = leaf.shard_ranges()
+            ref_ranges = ref.shard_ranges()
+            source_boxes = {}
+            for sh in tv.shards_of(ref.sharding):
+                source_boxes.setdefault(sh.ranges, sh.device)  # one replica per range
             for tdev, t in leaf.shards.items():
                 tr = t_ranges[tdev]
-                for sdev, sv in ref.shards.items():
-                    sr = s_ranges[sdev]
+                for sr, sdev in source_boxes.items():
                     hit = []
                     for (a0, ae), (b0, be) in zip(tr, sr):
                         lo, hi = max(a0, b0), min(a0 + ae, b0 + be)
@@ -1200,11 +1214,19 @@ def verify_restore(tv, state, out) -> tuple[int, int]:
                         hit.append((lo, hi - lo))
                     if hit is None:
                         continue
+                    sv = ref.shards.get(sdev)
+                    if sv is None:  # held by an equal-range replica here, or regenerate
+                        sv = next((ref.shards[d] for d, r in ref_ranges.items()
+                                   if r == sr and d in ref.shards), None)
+                    if sv is None:
+                        if path not in index:
+                            continue
+                        i, tname, dt = index[path]
+                        sv = gen_shard(i, tname, dt, sr, seed, t.device.index)
                     a = t[tuple(slice(o - to, o - to + e) for (o, e), (to, _) in zip(hit, tr))]
                     b = sv[tuple(slice(o - so, o - so + e) for (o, e), (so, _) in zip(hit, sr))]
                     if b.device != a.device:
                         b = b.to(a.device)
-                    ints = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
                     a, b = a.view(ints[a.element_size()]), b.view(ints[b.element_size()])
                     compared += a.numel() * a.element_size()
                     bad += 0 if torch.equal(a, b) else 1  # bit patterns (NaN-safe)
@@ -1498,6 +1520,9 @@ def main() -> None:
     ap.add_argument("--save-mode", default="async", choices=["async", "sync"],
                     help="async (default): each step's save is an async save + wait; sync: sync save")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--runtime", default="torchrun", choices=["torchrun", "threads"],
+                    help="--gpus N > 1 without torchrun: re-exec under torchrun (default, the driver's "
+                         "launch) or run N logical processes as threads of one process")
     ap.add_argument("--train-ms", type=float, default=1000.0)
     ap.add_argument("--c5-layers", type=int, default=8,
                     help="default line: Llama depth of the embedded C5 Checkpointer loop (0 = skip)")
@@ -1506,6 +1531,17 @@ def main() -> None:
                     help="default line: restores onto another sharding after the timed steps (0 = skip)")
     ap.add_argument("--inline-gc", action="store_true", help="c5: retention deletes inside wait() (reference)")
     args = ap.parse_args()
+    if (args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ
+            and args.runtime == "torchrun"):
+        # one process per GPU, exactly as the driver launches N > 1: re-exec under torchrun
+        import socket
+
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     if args.impl == "reference":
         d = Dist()
         if d.on and d.rank != 0:

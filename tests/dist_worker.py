@@ -66,6 +66,16 @@ def coord(base: str) -> None:
         assert sorted(tv.Checkpointer(rt, root).all_steps()) == [3, 4]
         got = ck.load_step()
         assert got["m"]["step"] == tv.Scalar("i64", 4)
+    # a job of fewer logical processes than ranks (restore onto fewer GPUs): every rank
+    # creates the subgroup, only its members get a runtime
+    sub = tv.DistributedRuntime.subgroup(backend, [0], barrier_timeout=90.0)
+    if rank == 0:
+        assert sub is not None and sub.process_count == 1 and sub.rank == 0
+        sub.local.barrier("sub")
+        assert sub.local.leader_broadcast("sub-nonce", b"x") == b"x"
+        assert sub.all_gather_object(7) == [7]
+    else:
+        assert sub is None
     ctx.barrier("done")
     dist.destroy_process_group()
 
@@ -196,6 +206,29 @@ def datapath(base: str) -> None:
         assert got == leaf[2].astype(np.float64).tobytes(), path
         n_cast += 1
     assert n_cast > 0
+    # restore onto FEWER processes than saved it (FSDP-world -> FSDP-1 on rank 0 only):
+    # the torchrun shape of "saved on 8, restored onto 4"
+    sub = tv.DistributedRuntime.subgroup(backend, [0], gpu=gpu, barrier_timeout=90.0)
+    if sub is not None:
+        mesh1 = tv.Mesh.create([("fsdp", 1)], process_count=1)
+        one_abs = {}
+        for path, leaf in leaves.items():
+            if path.startswith("extra/"):
+                continue
+            node = one_abs
+            parts = path.split("/")
+            for p in parts[:-1]:
+                node = node.setdefault(p, {})
+            node[parts[-1]] = tv.AbstractLeaf("array", leaf[2].shape, leaf[1], tv.Sharding(
+                mesh1, tv.PartitionSpec(("fsdp",) + (None,) * (leaf[2].ndim - 1)), leaf[2].shape))
+        out = tv.load_checkpoint(sub, "ck/run_1", {"state": one_abs}, tv.LoadOptions(mode="partial"))
+        for path, leaf in leaves.items():
+            if path.startswith("extra/"):
+                continue
+            node = out["state"]
+            for p in path.split("/"):
+                node = node[p]
+            assert tv.DenseArray(leaf[1], node.shards[0]).tobytes() == leaf[2].tobytes(), path
     rt.local.barrier("done")
     dist.destroy_process_group()
 

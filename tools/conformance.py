@@ -82,6 +82,7 @@ def main(argv: list[str]) -> int:
     sys.stdout = sys.stderr = log
     try:
         rc = pytest.main([dst, "-q", "-rfE", "-p", "no:cacheprovider", f"--junitxml={xml}",
+                          "--continue-on-collection-errors",
                           "--rootdir", work, "-o", "junit_family=xunit1", *argv])
     finally:
         sys.stdout, sys.stderr = old_out, old_err
