@@ -439,6 +439,7 @@ def run_ours(args) -> dict:
 
     import paper_2605_23066_b200 as tv
     from paper_2605_23066_b200 import native
+    from paper_2605_23066_b200.training_manager import delete_checkpoint
 
     d = Dist()
     d.init()
@@ -525,13 +526,19 @@ def run_ours(args) -> dict:
             nb, bad = verify_restore(tv, state, out, wl.leaves) if out is not None else (0, 0)
             verified["bytes_compared"] = int(d.sum(nb))
             verified["mismatched_boxes"] = int(d.sum(bad))
-        d.barrier()
         del out
+        # retire the checkpoint (counted in the step): process 0 deletes it as retention
+        # would — with recycling, its chunk files go to the recycle pool and the next
+        # save overwrites them in place (steady-state checkpointing with max_to_keep)
+        d.barrier()
+        tr = time.perf_counter()
         if d.rank == 0:
-            shutil.rmtree(os.path.join(base, path), ignore_errors=True)
+            delete_checkpoint(backend.store("retention"), path, recycle=args.recycle)
+            shutil.rmtree(os.path.join(base, path), ignore_errors=True)  # emptied dirs
+        retire_ms = d.max((time.perf_counter() - tr) * 1e3)
         d.barrier()
         return (ev0.elapsed_time(ev1), ev1.elapsed_time(ev2), (t1 - t0) * 1e3, (t2 - t1) * 1e3,
-                (tb - t0) * 1e3)
+                (tb - t0) * 1e3, retire_ms)
 
     for i in range(args.warmup):
         step(i)
@@ -541,13 +548,20 @@ def run_ours(args) -> dict:
     probe = {}
     if d.rank == 0:
         nthreads = min(128, len(os.sched_getaffinity(0)))
-        best = (0.0, 0.0)
+        best = (0.0, 0.0, 0.0)
         for _ in range(2):
-            w_gbs, r_gbs = native.probe_storage(base, nthreads, 1 << 30, 8 << 20)
-            best = (max(best[0], w_gbs), max(best[1], r_gbs))
-        probe["storage_write_GBps"], probe["storage_read_GBps"] = round(best[0], 2), round(best[1], 2)
+            w_gbs, rw_gbs, r_gbs = native.probe_storage_rewrite(base, nthreads, 1 << 30, 8 << 20)
+            best = (max(best[0], w_gbs), max(best[1], rw_gbs), max(best[2], r_gbs))
+        probe["storage_write_fresh_GBps"] = round(best[0], 2)
+        probe["storage_rewrite_GBps"] = round(best[1], 2)
+        # the save's storage roofline: fresh files, or files rewritten in place when the
+        # save overwrites recycled files
+        probe["storage_write_GBps"] = round(best[1] if args.recycle else best[0], 2)
+        probe["storage_read_GBps"] = round(best[2], 2)
         probe["storage_threads"] = nthreads
-        probe["storage_probe"] = f"{nthreads} threads x 1 GiB files, 8 MiB pwrite/pread from pinned memory, best of 2"
+        probe["storage_probe"] = (f"{nthreads} threads x 1 GiB files, 8 MiB pwrite/pread from pinned memory, "
+                                  "best of 2; write = " + ("rewrite of existing files (recycling on)"
+                                                           if args.recycle else "fresh files"))
     d.barrier()  # every rank probes its own link at the same time: the aggregate is concurrent
     d2h, h2d = native.probe_pcie(d.local if d.on else 0, 1 << 30, 3)
     probe["pcie_d2h_GBps_per_gpu"] = round(d2h, 2)
@@ -612,12 +626,13 @@ def run_ours(args) -> dict:
     before = native.totals()
     native.kernel_timing(True)
     timing = True
-    saves, restores, walls, blocks, host_blocks, snaps = [], [], [], [], [], []
+    saves, restores, walls, blocks, host_blocks, snaps, retires = [], [], [], [], [], [], []
     for i in range(args.steps):
-        s_ms, r_ms, ws, wr, b_ms = step(args.warmup + i)
+        s_ms, r_ms, ws, wr, b_ms, rt_ms = step(args.warmup + i)
         saves.append(d.max(s_ms))
         restores.append(d.max(r_ms))
-        walls.append(d.max(ws + wr))
+        retires.append(rt_ms)
+        walls.append(d.max(ws + wr) + rt_ms)
         host_blocks.append(d.max(b_ms))
         snaps.append(d.max(step_snap[-1]) if args.save_mode == "async" and step_snap else 0.0)
         blocks.append(host_blocks[-1] + snaps[-1])
@@ -663,7 +678,8 @@ def run_ours(args) -> dict:
     peer_gb = d.sum(after["peer_bytes"] - before["peer_bytes"]) / 1e9
     save_ms = statistics.mean(saves)
     restore_ms = statistics.mean(restores)
-    step_ms = save_ms + restore_ms
+    retire_ms = statistics.mean(retires)
+    step_ms = save_ms + restore_ms + retire_ms
     value = 2 * tree_bytes / (step_ms / 1e3) / 1e9
     save_gbs = tree_bytes / (save_ms / 1e3) / 1e9
     restore_gbs = tree_bytes / (restore_ms / 1e3) / 1e9
@@ -696,7 +712,7 @@ def run_ours(args) -> dict:
         # must fit the RAM-backed storage next to nothing else)
         del state
         torch.cuda.empty_cache()
-        c5 = c5_loop(tv, d, rt, N, base, args.c5_layers, args.c5_steps, args.train_ms)
+        c5 = c5_loop(tv, d, rt, N, base, args.c5_layers, args.c5_steps, args.train_ms, recycle=args.recycle)
 
     peaks = measured_peaks()
     result = {
@@ -724,6 +740,14 @@ def run_ours(args) -> dict:
         "restore_GBps": round(restore_gbs, 3),
         "save_ms": round(save_ms, 2),
         "restore_ms": round(restore_ms, 2),
+        "retire_ms": round(retire_ms, 2),
+        "recycle": {"enabled": bool(args.recycle),
+                    "files_overwritten_in_timed_steps": int(d.sum(after["save"]["recycled_files"]
+                                                                  - before["save"]["recycled_files"])),
+                    "note": "each step ends by retiring its checkpoint (process 0, inside the timed step); "
+                            "with recycling its chunk files go to the backend's recycle pool and the next "
+                            "save overwrites them in place (FilesystemBackend .tvpool; steady-state "
+                            "checkpointing with max_to_keep) instead of allocating fresh page-cache pages"},
         "wall_ms_per_step": round(statistics.mean(walls), 2),
         "save_mode": args.save_mode,
         "async_blocking_ms": round(blocking_ms + snap_dev_ms, 2),
@@ -833,7 +857,7 @@ def _pct(xs, q):
 
 
 def c5_loop(tv, d, rt, N: int, base: str, layers: int, steps: int, train_ms: float,
-            inline_gc: bool = False) -> dict:
+            inline_gc: bool = False, recycle: bool = True) -> dict:
     """C5 (BASELINE configs[4]): ``Checkpointer(keep_last=3)`` async save EVERY step of a
     synthetic training loop (fixed GPU time + an in-place update of every param shard);
     the blocking time is what the loop spends in ``save_step`` plus the snapshot
@@ -865,7 +889,7 @@ def c5_loop(tv, d, rt, N: int, base: str, layers: int, steps: int, train_ms: flo
     sync_save_ms = sync_ms[-1]
     cycles = int(train_ms * 1.965e6)
     ck = tv.Checkpointer(rt, "c5run", tv.RetentionPolicy(keep_last=3), tv.SaveOptions(sync=False),
-                         background_delete=not inline_gc)
+                         background_delete=not inline_gc, recycle=recycle)
     blocking, waits, joins, gcs, bg, snap_dev = [], [], [], [], [], []
     phase_sums: dict[str, float] = {}
     from paper_2605_23066_b200 import native
@@ -959,7 +983,7 @@ def run_c5(args) -> dict:
     d.barrier()
     backend = tv.FilesystemBackend(base)
     rt = open_runtime(tv, d, N, backend, gpus=list(range(N)))
-    res = c5_loop(tv, d, rt, N, base, args.layers, args.steps, args.train_ms, args.inline_gc)
+    res = c5_loop(tv, d, rt, N, base, args.layers, args.steps, args.train_ms, args.inline_gc, args.recycle)
     d.barrier()
     if d.rank == 0:
         shutil.rmtree(base, ignore_errors=True)
@@ -1281,11 +1305,14 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
                 for dev, t in _device_tensors(leaf):
                     host[(p, dev)].copy_(t, non_blocking=True)
         torch.cuda.synchronize()
-        dt = d.max(time.perf_counter() - t0)
         del out
         d.barrier()
-        if d.rank == 0:
-            shutil.rmtree(os.path.join(base, "e2e"), ignore_errors=True)
+        if d.rank == 0:  # retire it, as the main step does
+            from paper_2605_23066_b200.training_manager import delete_checkpoint
+
+            delete_checkpoint(rt.backend.store("retention"), path, recycle=args.recycle)
+        dt = d.max(time.perf_counter() - t0)
+        d.barrier()
         if i > 0:
             times.append(dt)
     del state, host
@@ -1301,8 +1328,8 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
         "sample": (f"the reference arm's sample: {len(e_leaves)} leaves"
                    + ("" if wl.name == "c1" else f" ({args.cpu_layers} layers + final_norm, no embed/lm_head)")),
         "config": wl.name,
-        "api": f"save_checkpoint({args.save_mode}) + wait() + load_checkpoint, with H2D of the inputs and "
-               "D2H of the restored shards (pinned) inside the timed region",
+        "api": f"save_checkpoint({args.save_mode}) + wait() + load_checkpoint + retire, with H2D of the "
+               "inputs and D2H of the restored shards (pinned) inside the timed region",
         "steps": args.e2e_steps,
     }
 
@@ -1520,6 +1547,8 @@ def main() -> None:
     ap.add_argument("--save-mode", default="async", choices=["async", "sync"],
                     help="async (default): each step's save is an async save + wait; sync: sync save")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-recycle", dest="recycle", action="store_false",
+                    help="retire each step's checkpoint by freeing its files instead of recycling them")
     ap.add_argument("--runtime", default="torchrun", choices=["torchrun", "threads"],
                     help="--gpus N > 1 without torchrun: re-exec under torchrun (default, the driver's "
                          "launch) or run N logical processes as threads of one process")

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TV_ABI_VERSION 1
+#define TV_ABI_VERSION 2
 #define TV_MAX_RANK 8
 
 #define TV_OK 0
@@ -134,6 +134,7 @@ typedef struct tv_stats {
   double seconds_io;            /* storage threads: time inside pwrite/pread (summed) */
   double seconds_wait_dma;      /* storage threads: time waiting for D2H/H2D events   */
   double seconds_wait_slot;     /* producer: time waiting for a free pinned slot      */
+  int64_t recycled_files;       /* save: outputs written over a recycled file (pool)  */
 } tv_stats;
 
 typedef struct tv_engine tv_engine;
@@ -174,6 +175,14 @@ int tv_engine_destroy(tv_engine* e);
  * thread (ctypes releases the GIL). */
 int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
                    const tv_output* outputs, int n_outputs, tv_stats* stats);
+/* tv_engine_save, drawing output files from a recycle pool (`pool_dir`, may be NULL):
+ * an output of N bytes claims a retired file `<pool_dir>/<N>/<name>` (rename to its
+ * `.partial`) and overwrites it in place — no page allocation or zeroing for storage
+ * that keeps its pages (tmpfs).  Steady-state checkpointing with retention
+ * (training_manager.py:262-295: a step is retired while the next is saved). */
+int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
+                          const tv_output* outputs, int n_outputs, const char* pool_dir,
+                          tv_stats* stats);
 
 /* Restore: fetch every item once, land it on its reader GPU, run its copies
  * (ChunkReader.read_range, chunkstore.py:507-593, _execute_reads + _assemble,
@@ -195,12 +204,22 @@ int tv_ipc_close(int device, uint64_t ptr);
  * interpreter lock).  ok[i] = 1 if paths[i] was removed, 0 if it did not exist; any other
  * failure returns TV_ERR_IO with the first failing path (training_manager.py:262-279). */
 int tv_unlink_many(const char* const* paths, int n, int n_threads, uint8_t* ok);
+/* Retire files into a recycle pool instead of unlinking them: each regular file moves to
+ * `<pool_dir>/<its size>/<unique name>` (same filesystem: a rename, pages kept); ok[i] as
+ * tv_unlink_many.  Files that cannot be renamed there are unlinked. */
+int tv_recycle_many(const char* const* paths, int n, const char* pool_dir, int n_threads,
+                    uint8_t* ok);
 
 /* ---- roofline probes (same run as the numbers they bound) ------------------------- */
 /* fio-style sequential write then read of n_threads files of file_bytes each, in
  * block_bytes pwrite/pread calls from pinned memory.  Files are removed afterwards. */
 int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
                      double* write_gbps, double* read_gbps);
+/* The storage probe plus a rewrite pass between write and read: the same files written
+ * again without truncation (pages already allocated: the recycled-file save path). */
+int tv_probe_storage_rewrite(const char* dir, int n_threads, int64_t file_bytes,
+                             int64_t block_bytes, double* write_gbps, double* rewrite_gbps,
+                             double* read_gbps);
 /* The same storage probe while a DMA thread keeps `device`'s copy engine busy for the
  * whole window (D2H during the writes, H2D during the reads): the contended rates of a
  * copy-through-pinned pipeline, whose DMA and page-cache copies share host memory. */

@@ -375,7 +375,7 @@ def as_device_region(values: Any, extents: tuple[int, ...], dtype: str, gpu: int
     else:
         from .treemodel import _host_storage
 
-        host = np.ascontiguousarray(_host_storage(values, dtype))
+        host = np.asarray(_host_storage(values, dtype), order="C")  # keeps 0-d arrays 0-d
         dev = torch.device("cuda", gpu if gpu is not None else torch.cuda.current_device())
         t = torch.from_numpy(host.view(np.uint8).reshape(-1)).to(dev)
         t = t.view(torch_dtype(dtype)).reshape(host.shape) if host.size else torch.empty(
@@ -410,15 +410,19 @@ class _PendingChunk:
 class ProcessArrayWriter:
     """Writes one process's chunks under ``<prefix>`` (``chunkstore.py:307-454``).
 
-    ``write_array`` only plans (keys, file offsets, duplicate checks); the bytes move in
-    ``flush`` — one native engine call for all arrays of the process — which ``finish``
-    runs before writing the manifest and ``array_metadata.json``.  Op order on the
-    backend is the reference's: chunk puts in write order, then manifest, then metadata.
+    ``write_array`` plans (keys, file offsets, duplicate checks); the bytes move in
+    ``flush`` — one native engine call for everything pending.  The save pipeline
+    builds its writer ``deferred``: every array of the process goes in ONE engine call
+    at ``finish`` (which then writes the manifest and ``array_metadata.json``).  A
+    writer used directly (``deferred=False``, the default) stores each array's chunks
+    before ``write_array`` returns, like the reference (aggregated: the data files that
+    are complete; the open one at ``finish``).  Op order on the backend is the
+    reference's: chunk puts in write order, then manifest, then metadata.
     """
 
     def __init__(self, store: Store, prefix: str, layout: str,
                  target_file_bytes: int = DEFAULT_TARGET_FILE_BYTES, *, engine_cfg=None,
-                 concurrent: int = 1):
+                 concurrent: int = 1, deferred: bool = False):
         if layout not in LAYOUTS:
             raise ChunkStoreError(f"unknown layout {layout!r}")
         self._store = store
@@ -435,6 +439,7 @@ class ProcessArrayWriter:
         self._finished = False
         self._engine_cfg = engine_cfg
         self._concurrent = concurrent
+        self._deferred = deferred
         self.stats = None
 
     def declare_array(self, leaf_path: str, meta: ArrayStorageMetadata,
@@ -485,7 +490,21 @@ class ProcessArrayWriter:
                 )
                 keys.append(self._plan_chunk(leaf_path, coords, region, box_off, meta.write_chunk,
                                              isz, nbytes))
+        if not self._deferred:
+            self._flush_complete()
         return keys
+
+    def _flush_complete(self) -> None:
+        """Store the pending chunks whose output is complete (per-leaf: all of them;
+        aggregated: those of data files before the open one)."""
+        if self._layout == PER_LEAF:
+            self.flush()
+            return
+        open_key = f"{self._prefix}/{DATA_DIR}/{self._fid}"
+        done = [p for p in self._pending if p.key != open_key]
+        if done:
+            self._pending = [p for p in self._pending if p.key == open_key]
+            self.stats = execute_writes(self._store, done, self._engine_cfg, self._concurrent)
 
     def _plan_chunk(self, leaf_path, coords, region, box_off, ext, isz, nbytes) -> str:
         ck = coords_key(coords)
@@ -593,8 +612,9 @@ def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, 
                 buf = np.empty(size, np.uint8)
                 host_bufs.append(buf)
                 outputs[i]["host"] = buf.ctypes.data if size else 0
+        pool = backend.recycle_pool() if root is not None else None
         with native.engine_lease(cfg, concurrent) as eng:
-            stats = eng.save(items, outputs)
+            stats = eng.save(items, outputs, pool)
         if root is not None:
             backend.record_bulk(store.identity, "put", out_keys, [0] * len(out_keys), sizes)
         else:
@@ -867,14 +887,22 @@ class ChunkReader:
         extents = tuple(e for _, e in ranges)
         gpu = self._gpu if self._gpu is not None else torch.cuda.current_device()
         out = torch.empty(extents, dtype=torch_dtype(meta.dtype), device=torch.device("cuda", gpu))
+        # the engine writes `out` on its own streams: the caching allocator may have handed
+        # back a block that work queued on the caller's stream still uses
+        torch.cuda.current_stream(gpu).synchronize()
         stats = ReadStats(bytes_requested=math.prod(extents) * isz)
-        if 0 in extents:
-            return out, stats
-        fetches = plan_fetches(self._prefix, leaf_path, self._arrays[leaf_path], meta, [ranges])
-        dest = Destination(gpu, out.data_ptr(), ranges, isz)
-        items = [FetchItem(f, gpu, [dest]) for f in fetches]
-        execute_reads(self._store, items, self._engine_cfg)
-        stats.bytes_loaded = sum(f.nbytes for f in fetches)
+        if 0 not in extents:
+            fetches = plan_fetches(self._prefix, leaf_path, self._arrays[leaf_path], meta, [ranges])
+            dest = Destination(gpu, out.data_ptr(), ranges, isz)
+            items = [FetchItem(f, gpu, [dest]) for f in fetches]
+            execute_reads(self._store, items, self._engine_cfg)
+            stats.bytes_loaded = sum(f.nbytes for f in fetches)
+        from . import compat
+
+        if compat.enabled():  # the reference's return type: a host numpy box
+            from .treemodel import DenseArray
+
+            return DenseArray(meta.dtype, out).to_numpy(), stats
         return out, stats
 
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <errno.h>
 #include <fcntl.h>
+#include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -25,7 +26,7 @@ const std::string& get_error() { return g_last_error; }
 
 int engine_create(int, int64_t, int64_t, int, tv_engine**);
 int engine_destroy(tv_engine*);
-int engine_save(tv_engine*, const tv_write_item*, int, const tv_output*, int, tv_stats*);
+int engine_save(tv_engine*, const tv_write_item*, int, const tv_output*, int, const char*, tv_stats*);
 int engine_load(tv_engine*, const tv_read_item*, int, const tv_input*, int, const tv_copy*, int,
                 tv_stats*);
 int copy_boxes(int, const tv_copy*, int, cudaStream_t);
@@ -95,7 +96,19 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
     tv::set_error("tv_engine_save: bad arguments");
     return TV_ERR_ARG;
   }
-  return tv::engine_save(e, items, n_items, outputs, n_outputs, stats);
+  return tv::engine_save(e, items, n_items, outputs, n_outputs, nullptr, stats);
+}
+
+int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
+                          const tv_output* outputs, int n_outputs, const char* pool_dir,
+                          tv_stats* stats) {
+  tv::DeviceGuard guard;
+  if (!e || n_items < 0 || n_outputs < 0) {
+    tv::set_error("tv_engine_save_pooled: bad arguments");
+    return TV_ERR_ARG;
+  }
+  return tv::engine_save(e, items, n_items, outputs, n_outputs,
+                         (pool_dir && pool_dir[0]) ? pool_dir : nullptr, stats);
 }
 
 int tv_engine_load(tv_engine* e, const tv_read_item* items, int n_items, const tv_input* inputs,
@@ -106,6 +119,60 @@ int tv_engine_load(tv_engine* e, const tv_read_item* items, int n_items, const t
     return TV_ERR_ARG;
   }
   return tv::engine_load(e, items, n_items, inputs, n_inputs, copies, n_copies, stats);
+}
+
+int tv_recycle_many(const char* const* paths, int n, const char* pool_dir, int n_threads,
+                    uint8_t* ok) {
+  if (n < 0 || (n > 0 && (!paths || !ok)) || !pool_dir || !pool_dir[0]) {
+    tv::set_error("tv_recycle_many: bad arguments");
+    return TV_ERR_ARG;
+  }
+  ::mkdir(pool_dir, 0777);
+  const int t = std::max(1, std::min(n_threads, std::max(1, n)));
+  static std::atomic<uint64_t> seq{0};
+  const uint64_t stamp = (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+  std::atomic<int> next{0};
+  std::atomic<int> failed{-1};
+  std::atomic<int> err_no{0};
+  auto work = [&] {
+    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) {
+      struct stat st;
+      if (::stat(paths[i], &st) != 0) {
+        ok[i] = 0;
+        if (errno != ENOENT && errno != ENOTDIR) {
+          int expect = -1;
+          if (failed.compare_exchange_strong(expect, i)) err_no.store(errno);
+        }
+        continue;
+      }
+      bool moved = false;
+      if (S_ISREG(st.st_mode) && st.st_size > 0) {
+        const std::string dir = std::string(pool_dir) + "/" + std::to_string((long long)st.st_size);
+        ::mkdir(dir.c_str(), 0777);  // EEXIST is fine
+        const std::string dst = dir + "/" + std::to_string((long long)::getpid()) + "-" +
+                                std::to_string(stamp) + "-" + std::to_string(seq.fetch_add(1));
+        moved = ::rename(paths[i], dst.c_str()) == 0;
+      }
+      if (moved || ::unlink(paths[i]) == 0) {
+        ok[i] = 1;
+      } else {
+        ok[i] = 0;
+        if (errno != ENOENT && errno != ENOTDIR) {
+          int expect = -1;
+          if (failed.compare_exchange_strong(expect, i)) err_no.store(errno);
+        }
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < t; ++k) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  if (failed.load() >= 0) {
+    tv::set_error(std::string("recycle ") + paths[failed.load()] + ": " + std::strerror(err_no.load()));
+    return TV_ERR_IO;
+  }
+  return TV_OK;
 }
 
 int tv_unlink_many(const char* const* paths, int n, int n_threads, uint8_t* ok) {
@@ -224,7 +291,7 @@ namespace {
 // returned too: the contended rates of a copy-through-pinned pipeline.
 int probe_storage_impl(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,
                        int device, double* write_gbps, double* read_gbps, double* d2h_gbps,
-                       double* h2d_gbps) {
+                       double* h2d_gbps, double* rewrite_gbps = nullptr) {
   if (!dir || n_threads < 1 || file_bytes < 1 || block_bytes < 1) {
     tv::set_error("tv_probe_storage: bad arguments");
     return TV_ERR_ARG;
@@ -253,6 +320,7 @@ int probe_storage_impl(const char* dir, int n_threads, int64_t file_bytes, int64
   }
   auto path = [&](int t) { return std::string(dir) + "/.tvgpu_probe_" + std::to_string(t); };
   std::atomic<int> failed{0};
+  bool truncate = true;  // false: overwrite the files the write pass left (recycled pages)
   auto run = [&](bool write, double* dma_gbps) {
     std::atomic<bool> stop{false};
     std::atomic<int64_t> moved{0};
@@ -275,7 +343,7 @@ int probe_storage_impl(const char* dir, int n_threads, int64_t file_bytes, int64
     double t0 = wall();
     for (int t = 0; t < n_threads; ++t)
       th.emplace_back([&, t] {
-        int fd = write ? ::open(path(t).c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644)
+        int fd = write ? ::open(path(t).c_str(), O_WRONLY | O_CREAT | (truncate ? O_TRUNC : 0) | O_CLOEXEC, 0644)
                        : ::open(path(t).c_str(), O_RDONLY | O_CLOEXEC);
         if (fd < 0) {
           failed = 1;
@@ -306,6 +374,11 @@ int probe_storage_impl(const char* dir, int n_threads, int64_t file_bytes, int64
     return gbps;
   };
   *write_gbps = run(true, d2h_gbps);
+  if (rewrite_gbps) {
+    truncate = false;
+    *rewrite_gbps = run(true, nullptr);
+    truncate = true;
+  }
   *read_gbps = run(false, h2d_gbps);
   for (int t = 0; t < n_threads; ++t) ::unlink(path(t).c_str());
   for (auto b : bufs) cudaFreeHost(b);
@@ -327,6 +400,17 @@ int tv_probe_storage(const char* dir, int n_threads, int64_t file_bytes, int64_t
                      double* write_gbps, double* read_gbps) {
   return probe_storage_impl(dir, n_threads, file_bytes, block_bytes, -1, write_gbps, read_gbps,
                             nullptr, nullptr);
+}
+
+int tv_probe_storage_rewrite(const char* dir, int n_threads, int64_t file_bytes,
+                             int64_t block_bytes, double* write_gbps, double* rewrite_gbps,
+                             double* read_gbps) {
+  if (!rewrite_gbps) {
+    tv::set_error("tv_probe_storage_rewrite: bad arguments");
+    return TV_ERR_ARG;
+  }
+  return probe_storage_impl(dir, n_threads, file_bytes, block_bytes, -1, write_gbps, read_gbps,
+                            nullptr, nullptr, rewrite_gbps);
 }
 
 int tv_probe_storage_dma(const char* dir, int n_threads, int64_t file_bytes, int64_t block_bytes,

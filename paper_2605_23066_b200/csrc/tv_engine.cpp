@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 #include <errno.h>
+#include <dirent.h>
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -560,11 +561,59 @@ struct OutputState {
   std::atomic<bool> committed{false};
 };
 
+// Recycled files (FilesystemBackend page recycling): `<pool>/<size>/<name>` are whole
+// files of exactly <size> bytes retired from older checkpoints.  An output of that size
+// claims one by renaming it to its `.partial` name and overwrites every byte in place:
+// the page cache already holds its pages, so the write skips page allocation and zeroing
+// (and, in a VM, the host's re-fault of pages returned by free-page reporting).
+class FilePool {
+ public:
+  explicit FilePool(std::string dir) : dir_(std::move(dir)) {}
+  bool empty() const { return dir_.empty(); }
+  // Move one pooled file of exactly `size` bytes to `dst`; false when none is left.
+  bool claim(int64_t size, const std::string& dst) {
+    Bucket* b = bucket(size);
+    for (;;) {
+      const size_t i = b->next.fetch_add(1);
+      if (i >= b->names.size()) return false;
+      if (::rename((b->dir + "/" + b->names[i]).c_str(), dst.c_str()) == 0) return true;
+    }
+  }
+
+ private:
+  struct Bucket {
+    std::string dir;
+    std::vector<std::string> names;
+    std::atomic<size_t> next{0};
+  };
+  Bucket* bucket(int64_t size) {
+    std::lock_guard<std::mutex> g(m_);
+    auto it = buckets_.find(size);
+    if (it != buckets_.end()) return it->second.get();
+    auto b = std::make_unique<Bucket>();
+    b->dir = dir_ + "/" + std::to_string(size);
+    if (DIR* d = ::opendir(b->dir.c_str())) {
+      while (struct dirent* ent = ::readdir(d)) {
+        if (ent->d_name[0] == '.') continue;
+        b->names.emplace_back(ent->d_name);
+      }
+      ::closedir(d);
+    }
+    Bucket* raw = b.get();
+    buckets_.emplace(size, std::move(b));
+    return raw;
+  }
+  std::string dir_;
+  std::mutex m_;
+  std::map<int64_t, std::unique_ptr<Bucket>> buckets_;
+};
+
 class SaveRun {
  public:
   SaveRun(tv_engine* e, const tv_write_item* items, int n_items, const tv_output* outs,
-          int n_outs, tv_stats* st)
-      : e_(e), items_(items), n_items_(n_items), n_outs_(n_outs), stats_(st) {
+          int n_outs, tv_stats* st, const char* pool_dir = nullptr)
+      : e_(e), items_(items), n_items_(n_items), n_outs_(n_outs), stats_(st),
+        pool_(pool_dir ? pool_dir : "") {
     outs_.reset(new OutputState[n_outs]);
     for (int i = 0; i < n_outs; ++i) {
       outs_[i].path = outs[i].path ? outs[i].path : "";
@@ -859,16 +908,7 @@ class SaveRun {
     if (o.path.empty()) {
       std::memcpy(o.host + w.file_off, host + w.slot_off, w.n);
     } else {
-      std::call_once(o.opened, [&] {
-        std::string err;
-        if (!dirs_.ensure(parent_of(o.path), err)) {
-          err_.set(TV_ERR_IO, err);
-          return;
-        }
-        std::string tmp = o.path + ".partial";
-        o.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0666);
-        if (o.fd < 0) err_.set(TV_ERR_IO, errno_msg("open", tmp));
-      });
+      std::call_once(o.opened, [&] { open_output(o); });
       if (o.fd < 0) return false;
       int64_t done = 0;
       while (done < w.n) {
@@ -886,6 +926,26 @@ class SaveRun {
     return true;
   }
 
+  // `<path>.partial`, write-only: a recycled file of the output's exact size when the
+  // pool has one (overwritten in full: run() checked every byte is produced), else new.
+  void open_output(OutputState& o) {
+    std::string err;
+    if (!dirs_.ensure(parent_of(o.path), err)) {
+      err_.set(TV_ERR_IO, err);
+      return;
+    }
+    std::string tmp = o.path + ".partial";
+    if (!pool_.empty() && o.size > 0 && pool_.claim(o.size, tmp)) {
+      o.fd = ::open(tmp.c_str(), O_WRONLY | O_CLOEXEC);
+      if (o.fd >= 0) {
+        recycled_ += 1;
+        return;
+      }
+    }
+    o.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0666);
+    if (o.fd < 0) err_.set(TV_ERR_IO, errno_msg("open", tmp));
+  }
+
   bool finish_output(int idx) {
     OutputState& o = outs_[idx];
     if (o.path.empty()) {
@@ -893,16 +953,7 @@ class SaveRun {
       return true;
     }
     if (o.size == 0) {
-      std::call_once(o.opened, [&] {
-        std::string err;
-        if (!dirs_.ensure(parent_of(o.path), err)) {
-          err_.set(TV_ERR_IO, err);
-          return;
-        }
-        std::string tmp = o.path + ".partial";
-        o.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0666);
-        if (o.fd < 0) err_.set(TV_ERR_IO, errno_msg("open", tmp));
-      });
+      std::call_once(o.opened, [&] { open_output(o); });
       if (o.fd < 0) return false;
     }
     if (::close(o.fd) != 0) {
@@ -940,6 +991,7 @@ class SaveRun {
     stats_->kernel_launches += stats_launches_.load();
     stats_->dma_copies += stats_dma_.load();
     stats_->files += files_.load();
+    stats_->recycled_files += recycled_.load();
     stats_->seconds_io += io_.seconds();
     stats_->seconds_wait_dma += wait_dma_.seconds();
     stats_->seconds_wait_slot += wait_slot_.seconds();
@@ -951,6 +1003,8 @@ class SaveRun {
   int n_items_;
   int n_outs_;
   tv_stats* stats_;
+  FilePool pool_;
+  std::atomic<int64_t> recycled_{0};
   std::unique_ptr<OutputState[]> outs_;
   Queue<int> free_slots_;
   std::vector<std::unique_ptr<Queue<SaveSlot>>> lanes_;
@@ -1328,10 +1382,10 @@ int engine_destroy(tv_engine* e) {
 }
 
 int engine_save(tv_engine* e, const tv_write_item* items, int n_items, const tv_output* outputs,
-                int n_outputs, tv_stats* stats) {
+                int n_outputs, const char* pool_dir, tv_stats* stats) {
   std::lock_guard<std::mutex> g(e->call_m);
   tv_stats local{};
-  SaveRun run(e, items, n_items, outputs, n_outputs, stats ? stats : &local);
+  SaveRun run(e, items, n_items, outputs, n_outputs, stats ? stats : &local, pool_dir);
   int rc = run.run();
   run.publish_stats();
   return rc;

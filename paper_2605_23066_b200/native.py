@@ -58,7 +58,7 @@ STATS = np.dtype(
     [("bytes_device", "<i8"), ("bytes_storage", "<i8"), ("bytes_packed", "<i8"),
      ("kernel_launches", "<i8"), ("dma_copies", "<i8"), ("files", "<i8"),
      ("seconds_total", "<f8"), ("seconds_kernel", "<f8"), ("seconds_io", "<f8"),
-     ("seconds_wait_dma", "<f8"), ("seconds_wait_slot", "<f8")],
+     ("seconds_wait_dma", "<f8"), ("seconds_wait_slot", "<f8"), ("recycled_files", "<i8")],
     align=True,
 )
 
@@ -68,7 +68,8 @@ EXPORTS = (
     "tv_kernel_timing_collect", "tv_engine_create",
     "tv_engine_destroy", "tv_engine_save", "tv_engine_load", "tv_enable_peer_access",
     "tv_ipc_export", "tv_ipc_import", "tv_ipc_close", "tv_probe_storage", "tv_probe_pcie",
-    "tv_unlink_many", "tv_probe_storage_dma",
+    "tv_unlink_many", "tv_probe_storage_dma", "tv_engine_save_pooled", "tv_recycle_many",
+    "tv_probe_storage_rewrite",
 )
 
 _lib = None
@@ -96,6 +97,10 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tv_probe_storage": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "tv_probe_pcie": (I, [I, L, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "tv_unlink_many": (I, [P, I, I, P]),
+        "tv_engine_save_pooled": (I, [P, P, I, P, I, ctypes.c_char_p, P]),
+        "tv_recycle_many": (I, [P, I, ctypes.c_char_p, I, P]),
+        "tv_probe_storage_rewrite": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D),
+                                         ctypes.POINTER(D)]),
         "tv_probe_storage_dma": (I, [ctypes.c_char_p, I, L, L, I, ctypes.POINTER(D), ctypes.POINTER(D),
                                      ctypes.POINTER(D), ctypes.POINTER(D)]),
     }
@@ -122,7 +127,7 @@ def lib() -> ctypes.CDLL:
             except OSError as exc:
                 raise NativeError(f"cannot load {LIB_PATH}: {exc}") from exc
             _declare(handle)
-            if handle.tv_abi_version() != 1:
+            if handle.tv_abi_version() != 2:
                 raise NativeError("libtvgpu ABI version mismatch")
             _lib = handle
     return _lib
@@ -217,7 +222,7 @@ def write_table(src_base, src_shape, src_off, ext, itemsize, file, device, file_
 # Process-wide counters of native work (bench.py reports the kernel launches and DMA
 # transfers its timed region issued).
 _FIELDS = ("kernel_launches", "dma_copies", "bytes_device", "bytes_storage", "bytes_packed", "files",
-           "seconds_total", "seconds_io", "seconds_wait_dma", "seconds_wait_slot")
+           "seconds_total", "seconds_io", "seconds_wait_dma", "seconds_wait_slot", "recycled_files")
 TOTALS = {"save": dict.fromkeys(_FIELDS, 0), "load": dict.fromkeys(_FIELDS, 0),
           "kernels": {"kernel_launches": 0}, "peer": {"bytes": 0}}
 _totals_lock = threading.Lock()
@@ -309,6 +314,19 @@ def unlink_many(paths: Sequence[str], threads: int) -> list[bool]:
     return [bool(x) for x in ok]
 
 
+def recycle_many(paths: Sequence[str], pool_dir: str, threads: int) -> list[bool]:
+    """Retire files into the recycle pool ``pool_dir`` (``<pool_dir>/<size>/<name>``,
+    renamed on native threads; unrenameable files are unlinked).  True = retired, False =
+    did not exist.  Raises BackendError on any other failure."""
+    if not paths:
+        return []
+    table = PathTable(list(paths))
+    ok = np.zeros(len(paths), np.uint8)
+    check(lib().tv_recycle_many(table.pointers.ctypes.data, len(paths), pool_dir.encode(), int(threads),
+                                ok.ctypes.data), "tv_recycle_many")
+    return [bool(x) for x in ok]
+
+
 def probe_storage(directory: str, threads: int, file_bytes: int, block_bytes: int) -> tuple[float, float]:
     w, r = ctypes.c_double(), ctypes.c_double()
     check(
@@ -317,6 +335,16 @@ def probe_storage(directory: str, threads: int, file_bytes: int, block_bytes: in
         "tv_probe_storage",
     )
     return w.value, r.value
+
+
+def probe_storage_rewrite(directory: str, threads: int, file_bytes: int,
+                          block_bytes: int) -> tuple[float, float, float]:
+    """(fresh write, rewrite in place, read) GB/s on the same files."""
+    w, rw, r = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    check(lib().tv_probe_storage_rewrite(directory.encode(), threads, file_bytes, block_bytes,
+                                         ctypes.byref(w), ctypes.byref(rw), ctypes.byref(r)),
+          "tv_probe_storage_rewrite")
+    return w.value, rw.value, r.value
 
 
 def probe_storage_dma(directory: str, threads: int, file_bytes: int, block_bytes: int,
@@ -371,13 +399,15 @@ class Engine:
             lib().tv_engine_destroy(self._h)
             self._h = None
 
-    def save(self, items: np.ndarray, outputs: np.ndarray) -> np.ndarray:
+    def save(self, items: np.ndarray, outputs: np.ndarray, pool_dir: str | None = None) -> np.ndarray:
+        """Write every item into its output; with ``pool_dir`` outputs reuse recycled
+        files of their exact size (see tv_engine_save_pooled)."""
         stats = np.zeros(1, STATS)
         items = np.ascontiguousarray(items, WRITE_ITEM)
         outputs = np.ascontiguousarray(outputs, OUTPUT)
         with _bound_to(self.cpus):
-            rc = lib().tv_engine_save(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
-                                      stats.ctypes.data)
+            rc = lib().tv_engine_save_pooled(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
+                                             pool_dir.encode() if pool_dir else None, stats.ctypes.data)
         _account("save", stats[0])
         check(rc, "tv_engine_save")
         return stats[0]

@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
                          capture_output=True, text=True, check=True).stdout
     exported = set(re.findall(r"\bT (tv_\w+)", out))
     assert declared <= exported
-    assert lib.tv_abi_version() == 1
+    assert lib.tv_abi_version() == 2
 
 
 def test_struct_layouts_match_numpy_dtypes(tmp_path):

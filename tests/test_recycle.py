@@ -1,0 +1,58 @@
+"""Recycle pool of the filesystem backend (host side, CPU): retention deletes with
+``recycle=True`` retire chunk payload files into ``<root>/.tvpool/<size>/`` (metadata
+documents are unlinked), the pool is invisible to listings and reserved as a key, and
+``drain_recycle_pool`` frees it.  The engine side (saves overwriting pooled files) is
+tests/test_recycle_gpu.py."""
+
+from __future__ import annotations
+
+import os
+
+import pytest
+
+import paper_2605_23066_b200 as tv
+from paper_2605_23066_b200.errors import BackendError
+from paper_2605_23066_b200.training_manager import delete_checkpoint
+
+
+def _checkpoint(store, prefix):
+    store.put(f"{prefix}/global_metadata.json", b"{}")
+    store.put(f"{prefix}/process_0/array_metadata.json", b"{}")
+    store.put(f"{prefix}/process_0/m/w/c.0.0", b"x" * 4096)
+    store.put(f"{prefix}/process_0/m/w/c.1.0", b"y" * 4096)
+    store.put(f"{prefix}/process_0/d/0", b"z" * 1000)
+
+
+def test_recycle_retires_payloads_and_hides_the_pool(tmp_path):
+    backend = tv.FilesystemBackend(tmp_path)
+    store = backend.store()
+    _checkpoint(store, "run/step_00000001")
+    assert backend.recycle_pool() is None
+    delete_checkpoint(store, "run/step_00000001", recycle=True)
+    assert store.list_keys("") == []
+    pool = backend.recycle_pool()
+    assert pool is not None and os.path.basename(pool) == ".tvpool"
+    sizes = sorted((d, len(os.listdir(os.path.join(pool, d)))) for d in os.listdir(pool))
+    assert sizes == [("1000", 1), ("4096", 2)]  # payload files only, grouped by size
+    assert backend.recycle_pool_bytes() == 2 * 4096 + 1000
+    assert not (tmp_path / "run" / "step_00000001").exists()  # emptied dirs pruned
+    with pytest.raises(BackendError):
+        store.put(".tvpool/x", b"1")
+    assert backend.drain_recycle_pool() == 2 * 4096 + 1000
+    assert backend.recycle_pool() is None
+
+
+def test_plain_delete_frees(tmp_path):
+    backend = tv.FilesystemBackend(tmp_path)
+    store = backend.store()
+    _checkpoint(store, "ck")
+    delete_checkpoint(store, "ck")
+    assert backend.recycle_pool() is None and store.list_keys("") == []
+
+
+def test_memory_backend_ignores_recycle():
+    backend = tv.MemoryBackend()
+    store = backend.store()
+    _checkpoint(store, "ck")
+    delete_checkpoint(store, "ck", recycle=True)
+    assert store.list_keys("") == [] and backend.recycle_pool() is None
