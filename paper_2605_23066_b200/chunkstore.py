@@ -377,7 +377,7 @@ def as_device_region(values: Any, extents: tuple[int, ...], dtype: str, gpu: int
 
         host = np.asarray(_host_storage(values, dtype), order="C")  # keeps 0-d arrays 0-d
         dev = torch.device("cuda", gpu if gpu is not None else torch.cuda.current_device())
-        t = torch.from_numpy(host.view(np.uint8).reshape(-1)).to(dev)
+        t = torch.from_numpy(host.reshape(-1).view(np.uint8)).to(dev)
         t = t.view(torch_dtype(dtype)).reshape(host.shape) if host.size else torch.empty(
             host.shape, dtype=torch_dtype(dtype), device=dev)
     if tuple(t.shape) != tuple(extents):

@@ -69,10 +69,9 @@ def test_checkpointer_recycle_loop(tmp_path):
         for t in shards.values():
             t.fill_(float(step))
         ck.save_step(step, {"m": {"w": leaf}}, {"m": {"w": s}})
-    ck.wait()
+    ck.close()  # joins the save and the background retention, drains the pool
     assert ck.all_steps() == [4, 5]
+    assert backend.recycle_pool() is None
     for step in (4, 5):
         out = ck.load_step(step, options=tv.LoadOptions(to_host=True), current_mesh=mesh)
         assert np.all(out["m"]["w"].data == float(step))
-    ck.close()
-    assert backend.recycle_pool() is None  # close() drained the pool
