@@ -674,6 +674,8 @@ def run_ours(args) -> dict:
             "pcie_GB": round((a["bytes_device"] - b["bytes_device"]) / 1e9, 3),
             # save: bytes packed by the kernel; load: bytes the unpack / NVLink fan-out moved
             "kernel_GB": round((a["bytes_packed"] - b["bytes_packed"]) / 1e9, 3),
+            # bytes DMA'd straight into / out of registered recycled files (no pinned slot)
+            "zero_copy_GB": round((a["zero_copy_bytes"] - b["zero_copy_bytes"]) / 1e9, 3),
         }
     peer_gb = d.sum(after["peer_bytes"] - before["peer_bytes"]) / 1e9
     save_ms = statistics.mean(saves)

@@ -135,6 +135,7 @@ typedef struct tv_stats {
   double seconds_wait_dma;      /* storage threads: time waiting for D2H/H2D events   */
   double seconds_wait_slot;     /* producer: time waiting for a free pinned slot      */
   int64_t recycled_files;       /* save: outputs written over a recycled file (pool)  */
+  int64_t zero_copy_bytes;      /* bytes DMA'd straight into / out of registered file pages */
 } tv_stats;
 
 typedef struct tv_engine tv_engine;
@@ -209,6 +210,18 @@ int tv_unlink_many(const char* const* paths, int n, int n_threads, uint8_t* ok);
  * tv_unlink_many.  Files that cannot be renamed there are unlinked. */
 int tv_recycle_many(const char* const* paths, int n, const char* pool_dir, int n_threads,
                     uint8_t* ok);
+
+/* Zero-copy recycle pool: map (MAP_SHARED) and register with CUDA every file of the
+ * pool on a RAM-backed filesystem that is not registered yet.  A registered file keeps
+ * its registration while it cycles pool -> checkpoint -> pool, and saves / restores then
+ * DMA straight into / out of its page-cache pages.  No GPU: returns TV_OK, 0 bytes. */
+int tv_pool_register(const char* pool_dir, int n_threads, int64_t* registered_bytes);
+/* Release the registrations of, and unlink, every pool file. */
+int tv_pool_drain(const char* pool_dir, int64_t* freed_bytes);
+/* Registered mappings held by this process (files, bytes). */
+int tv_mapping_stats(int64_t* files, int64_t* bytes);
+/* Release every registered mapping (the files stay). */
+int tv_mapping_release_all(void);
 
 /* ---- roofline probes (same run as the numbers they bound) ------------------------- */
 /* fio-style sequential write then read of n_threads files of file_bytes each, in

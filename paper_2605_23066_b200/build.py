@@ -19,7 +19,7 @@ INCLUDE = REPO / "include"
 LIB = PKG / "libtvgpu.so"
 OBJ = REPO / "build" / "tvgpu"
 
-SOURCES = ["tv_copy.cu", "tv_cast.cu", "tv_engine.cpp", "tv_capi.cpp"]
+SOURCES = ["tv_copy.cu", "tv_cast.cu", "tv_engine.cpp", "tv_capi.cpp", "tv_mapped.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-Wall", f"-I{INCLUDE}"]
 

@@ -153,6 +153,7 @@ int tv_recycle_many(const char* const* paths, int n, const char* pool_dir, int n
                                 std::to_string(stamp) + "-" + std::to_string(seq.fetch_add(1));
         moved = ::rename(paths[i], dst.c_str()) == 0;
       }
+      if (!moved) tv::mapping_release_path(paths[i]);
       if (moved || ::unlink(paths[i]) == 0) {
         ok[i] = 1;
       } else {
@@ -186,6 +187,7 @@ int tv_unlink_many(const char* const* paths, int n, int n_threads, uint8_t* ok) 
   std::atomic<int> err_no{0};
   auto work = [&] {
     for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) {
+      tv::mapping_release_path(paths[i]);  // a registered file: drop its mapping first
       if (::unlink(paths[i]) == 0) {
         ok[i] = 1;
       } else {

@@ -436,6 +436,7 @@ int dma_streams() {
 struct DeviceCtx {
   int device = -1;
   std::vector<cudaStream_t> streams;
+  cudaStream_t zero_copy = nullptr;  // DMA straight into / out of registered file pages
   std::unique_ptr<JobUploader> uploader;
   std::unique_ptr<StagingPool> staging;
   cudaStream_t stream_for(int64_t k) const { return streams[(size_t)(k % (int64_t)streams.size())]; }
@@ -469,6 +470,7 @@ int device_ctx(tv_engine* e, int device, DeviceCtx** out) {
     TV_CUDA_CHECK(cudaSetDevice(device));
     ctx->streams.resize(dma_streams());
     for (auto& st : ctx->streams) TV_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    TV_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->zero_copy, cudaStreamNonBlocking));
     ctx->uploader = std::make_unique<JobUploader>(device);
     ctx->staging = std::make_unique<StagingPool>(device, e->staging_bytes);
     int rc = ctx->staging->init();
@@ -554,6 +556,8 @@ struct SaveSlot {
 struct OutputState {
   std::string path;   // empty → host buffer
   char* host = nullptr;
+  char* mapped = nullptr;  // registered page-cache mapping of a claimed recycled file
+  int64_t direct = 0;      // bytes DMA'd straight into `mapped`
   int64_t size = 0;
   std::atomic<int64_t> left{0};
   std::once_flag opened;
@@ -621,6 +625,7 @@ class SaveRun {
       outs_[i].size = outs[i].size;
       outs_[i].left.store(outs[i].size);
     }
+    claimed_.assign(n_outs > 0 ? n_outs : 1, 0);
   }
 
   int run() {
@@ -649,15 +654,20 @@ class SaveRun {
       }
     }
     for (int s = 0; s < e_->n_slots; ++s) free_slots_.push(s);
+    direct_.assign(n_items_, 0);
+    if (!pool_.empty() && mappings_exist()) claim_outputs();
     assign_lanes();
     std::vector<std::thread> writers;
     for (int t = 0; t < (int)lanes_.size(); ++t) writers.emplace_back([this, t] { writer_loop(t); });
     // Zero-byte outputs are committed up front.
     for (int o = 0; o < n_outs_; ++o)
       if (outs_[o].size == 0) finish_output(o);
+    std::thread finisher;
+    if (!err_.failed.load() && issue_direct()) finisher = std::thread([this] { finish_direct(); });
     produce();
     for (auto& q : lanes_) q->close();
     for (auto& w : writers) w.join();
+    if (finisher.joinable()) finisher.join();
     for (auto& ev : events_) cudaEventDestroy(ev);
     if (err_.failed.load()) {
       abort_outputs();
@@ -683,6 +693,86 @@ class SaveRun {
     bool finished() const { return pos >= items.size(); }
   };
 
+  // Zero-copy path (registered recycle pool, tv_mapped.cpp).  Outputs are opened up
+  // front: each claims a recycled file of its size; when that file's pages are
+  // registered, every contiguous item of the output is DMA'd straight into them and
+  // never touches a pinned slot or a writer thread.
+  void claim_outputs() {
+    for (int o = 0; o < n_outs_ && !err_.failed.load(); ++o) {
+      OutputState& out = outs_[o];
+      if (out.path.empty() || out.size == 0) continue;
+      std::call_once(out.opened, [&] { open_output(out); });
+      if (out.fd >= 0 && claimed_[o]) out.mapped = mapping_for_fd(out.fd, out.size);
+    }
+    for (int i = 0; i < n_items_; ++i) {
+      const auto& it = items_[i];
+      const int64_t n = box_bytes(it.ext, it.rank, it.itemsize);
+      int64_t boff = 0, bn = 0;
+      if (n > 0 && outs_[it.file].mapped && box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn))
+        direct_[i] = 1;
+    }
+  }
+
+  // D2H of every direct item on its device's zero-copy stream; one event per device.
+  bool issue_direct() {
+    std::map<int, cudaStream_t> used;
+    for (int i = 0; i < n_items_; ++i) {
+      if (!direct_[i]) continue;
+      const auto& it = items_[i];
+      DeviceCtx* ctx = nullptr;
+      int rc = device_ctx(e_, it.device, &ctx);
+      if (rc != TV_OK) {
+        err_.set(rc, get_error());
+        return false;
+      }
+      cudaSetDevice(it.device);
+      int64_t boff = 0, bn = 0;
+      box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn);
+      const char* src = reinterpret_cast<const char*>(it.src.base) + boff;
+      OutputState& o = outs_[it.file];
+      if (cudaMemcpyAsync(o.mapped + it.file_off, src, bn, cudaMemcpyDefault, ctx->zero_copy) !=
+          cudaSuccess) {
+        err_.set(TV_ERR_CUDA, std::string("zero-copy D2H: ") + cudaGetErrorString(cudaGetLastError()));
+        return false;
+      }
+      o.direct += bn;
+      used[it.device] = ctx->zero_copy;
+      stats_dma_ += 1;
+      stats_bytes_device_ += bn;
+    }
+    for (auto& kv : used) {
+      cudaSetDevice(kv.first);
+      cudaEvent_t ev;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventRecord(ev, kv.second) != cudaSuccess) {
+        err_.set(TV_ERR_CUDA, "zero-copy event");
+        return false;
+      }
+      direct_events_.push_back({kv.first, ev});
+    }
+    return !direct_events_.empty();
+  }
+
+  // When the direct DMAs have landed: count their bytes; outputs complete -> commit.
+  void finish_direct() {
+    for (auto& de : direct_events_) {
+      cudaSetDevice(de.first);
+      const double t0 = now_s();
+      cudaError_t ce = cudaEventSynchronize(de.second);
+      wait_dma_.add(now_s() - t0);
+      cudaEventDestroy(de.second);
+      if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("zero-copy D2H: ") + cudaGetErrorString(ce));
+    }
+    if (err_.failed.load()) return;
+    for (int o = 0; o < n_outs_; ++o) {
+      OutputState& out = outs_[o];
+      if (!out.mapped || out.direct == 0) continue;
+      stats_bytes_storage_ += out.direct;
+      zero_copy_bytes_ += out.direct;
+      if (out.left.fetch_sub(out.direct) == out.direct && !finish_output(o)) return;
+    }
+  }
+
   void assign_lanes() {
     const int L = std::max(1, e_->n_threads);
     lanes_.clear();
@@ -703,7 +793,8 @@ class SaveRun {
       lane_of_[o] = best;
       load[best] += std::max<int64_t>(outs_[o].size, 1);
     }
-    for (int i = 0; i < n_items_; ++i) cursors_[lane_of_[items_[i].file]].items.push_back(i);
+    for (int i = 0; i < n_items_; ++i)
+      if (!direct_[i]) cursors_[lane_of_[items_[i].file]].items.push_back(i);
   }
 
   // Fill slot `cur` from lane `k`; returns false on error.
@@ -939,6 +1030,7 @@ class SaveRun {
       o.fd = ::open(tmp.c_str(), O_WRONLY | O_CLOEXEC);
       if (o.fd >= 0) {
         recycled_ += 1;
+        claimed_[&o - outs_.get()] = 1;
         return;
       }
     }
@@ -956,6 +1048,7 @@ class SaveRun {
       std::call_once(o.opened, [&] { open_output(o); });
       if (o.fd < 0) return false;
     }
+    if (o.mapped) ::futimens(o.fd, nullptr);  // DMA'd bytes do not touch the mtime
     if (::close(o.fd) != 0) {
       err_.set(TV_ERR_IO, errno_msg("close", o.path));
       return false;
@@ -976,6 +1069,7 @@ class SaveRun {
       OutputState& o = outs_[i];
       if (o.path.empty() || o.committed.load()) continue;
       if (o.fd >= 0) {
+        if (o.mapped) mapping_release_fd(o.fd);  // its pages go with the file
         ::close(o.fd);
         o.fd = -1;
         ::unlink((o.path + ".partial").c_str());
@@ -992,6 +1086,7 @@ class SaveRun {
     stats_->dma_copies += stats_dma_.load();
     stats_->files += files_.load();
     stats_->recycled_files += recycled_.load();
+    stats_->zero_copy_bytes += zero_copy_bytes_.load();
     stats_->seconds_io += io_.seconds();
     stats_->seconds_wait_dma += wait_dma_.seconds();
     stats_->seconds_wait_slot += wait_slot_.seconds();
@@ -1004,7 +1099,10 @@ class SaveRun {
   int n_outs_;
   tv_stats* stats_;
   FilePool pool_;
-  std::atomic<int64_t> recycled_{0};
+  std::atomic<int64_t> recycled_{0}, zero_copy_bytes_{0};
+  std::vector<char> claimed_;                      // output claimed a recycled file
+  std::vector<char> direct_;                       // item DMA'd straight into its mapping
+  std::vector<std::pair<int, cudaEvent_t>> direct_events_;
   std::unique_ptr<OutputState[]> outs_;
   Queue<int> free_slots_;
   std::vector<std::unique_ptr<Queue<SaveSlot>>> lanes_;
@@ -1028,6 +1126,7 @@ struct InputState {
   int64_t size = 0;
   std::once_flag opened;
   int fd = -1;
+  const char* mapped = nullptr;  // registered page-cache mapping (zero-copy H2D source)
 };
 
 struct ItemState {
@@ -1111,6 +1210,7 @@ class LoadRun {
     stats_->kernel_launches += launches_.load();
     stats_->dma_copies += dma_.load();
     stats_->files += files_.load();
+    stats_->zero_copy_bytes += zero_copy_bytes_.load();
     stats_->seconds_io += io_.seconds();
     stats_->seconds_wait_dma += wait_dma_.seconds();
     stats_->seconds_wait_slot += wait_slot_.seconds();
@@ -1165,6 +1265,15 @@ class LoadRun {
         st.staged_off = off;
         st.base = ctx->staging->base() + off;
       }
+      if (maps_ && ins_[it.input].host == nullptr) {
+        InputState& in = ins_[it.input];
+        std::call_once(in.opened, [&] { open_input(in); });
+        if (err_.failed.load()) return;
+        if (in.mapped) {
+          if (!run_mapped(i, in.mapped)) return;
+          continue;
+        }
+      }
       const int pieces = (int)((it.nbytes + cap - 1) / cap);
       st.left.store(pieces);
       for (int p = 0; p < pieces; ++p) {
@@ -1190,11 +1299,7 @@ class LoadRun {
       std::memcpy(dst, in.host + off, n);
       return true;
     }
-    std::call_once(in.opened, [&] {
-      in.fd = ::open(in.path.c_str(), O_RDONLY | O_CLOEXEC);
-      if (in.fd < 0) err_.set(TV_ERR_IO, errno_msg("open", in.path));
-      else files_ += 1;
-    });
+    std::call_once(in.opened, [&] { open_input(in); });
     if (in.fd < 0) return false;
     int64_t done = 0;
     while (done < n) {
@@ -1211,6 +1316,37 @@ class LoadRun {
       done += r;
     }
     return true;
+  }
+
+  void open_input(InputState& in) {
+    in.fd = ::open(in.path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (in.fd < 0) {
+      err_.set(TV_ERR_IO, errno_msg("open", in.path));
+      return;
+    }
+    files_ += 1;
+    if (maps_) in.mapped = mapping_for_fd(in.fd, in.size);
+  }
+
+  // Zero-copy restore of an item whose file is a registered mapping: H2D straight from
+  // the page-cache pages (no pread, no slot), then its copies, on the item's stream.
+  bool run_mapped(int i, const char* src) {
+    const auto& it = items_[i];
+    ItemState& st = states_[i];
+    DeviceCtx* ctx = ctx_for(it.device);
+    if (!ctx) return false;
+    cudaSetDevice(it.device);
+    cudaStream_t stream = ctx->stream_for(i);
+    if (cudaMemcpyAsync(st.base, src + it.in_off, it.nbytes, cudaMemcpyDefault, stream) != cudaSuccess) {
+      err_.set(TV_ERR_CUDA, std::string("zero-copy H2D: ") + cudaGetErrorString(cudaGetLastError()));
+      return false;
+    }
+    dma_ += 1;
+    bytes_device_ += it.nbytes;
+    bytes_storage_ += it.nbytes;
+    zero_copy_bytes_ += it.nbytes;
+    launch_copies(i);
+    return !err_.failed.load();
   }
 
   // Returns true when the slot has been handed back to the free list.
@@ -1303,8 +1439,9 @@ class LoadRun {
   std::mutex used_m_;
   std::map<int, DeviceCtx*> used_devices_;
   std::atomic<int64_t> bytes_device_{0}, bytes_storage_{0}, bytes_packed_{0}, launches_{0},
-      dma_{0}, files_{0};
+      dma_{0}, files_{0}, zero_copy_bytes_{0};
   Clock io_, wait_dma_, wait_slot_;
+  const bool maps_ = mappings_exist();  // any registered file mapping in this process
 };
 
 }  // namespace
@@ -1365,9 +1502,11 @@ int engine_destroy(tv_engine* e) {
     for (auto& kv : e->devices) {
       cudaSetDevice(kv.first);
       for (cudaStream_t st : kv.second->streams) cudaStreamSynchronize(st);
+      if (kv.second->zero_copy) cudaStreamSynchronize(kv.second->zero_copy);
       kv.second->uploader.reset();
       kv.second->staging.reset();
       for (cudaStream_t st : kv.second->streams) cudaStreamDestroy(st);
+      if (kv.second->zero_copy) cudaStreamDestroy(kv.second->zero_copy);
     }
     e->devices.clear();
   }

@@ -95,4 +95,11 @@ cudaError_t launch_cast_jobs(const CastJob* dev_jobs, const CastJob* host_jobs, 
 bool box_contiguous(const tv_array_box& b, const int64_t* ext, int rank, int itemsize,
                     int64_t* byte_off, int64_t* nbytes);
 
+// Registered file mappings (tv_mapped.cpp): the registered, MAP_SHARED mapping of the
+// file open as `fd` when its inode is in the cache with exactly `size` bytes, else null.
+char* mapping_for_fd(int fd, int64_t size);
+bool mappings_exist();
+void mapping_release_fd(int fd);
+void mapping_release_path(const char* path);
+
 }  // namespace tv

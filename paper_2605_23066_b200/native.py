@@ -58,7 +58,8 @@ STATS = np.dtype(
     [("bytes_device", "<i8"), ("bytes_storage", "<i8"), ("bytes_packed", "<i8"),
      ("kernel_launches", "<i8"), ("dma_copies", "<i8"), ("files", "<i8"),
      ("seconds_total", "<f8"), ("seconds_kernel", "<f8"), ("seconds_io", "<f8"),
-     ("seconds_wait_dma", "<f8"), ("seconds_wait_slot", "<f8"), ("recycled_files", "<i8")],
+     ("seconds_wait_dma", "<f8"), ("seconds_wait_slot", "<f8"), ("recycled_files", "<i8"),
+     ("zero_copy_bytes", "<i8")],
     align=True,
 )
 
@@ -69,7 +70,8 @@ EXPORTS = (
     "tv_engine_destroy", "tv_engine_save", "tv_engine_load", "tv_enable_peer_access",
     "tv_ipc_export", "tv_ipc_import", "tv_ipc_close", "tv_probe_storage", "tv_probe_pcie",
     "tv_unlink_many", "tv_probe_storage_dma", "tv_engine_save_pooled", "tv_recycle_many",
-    "tv_probe_storage_rewrite",
+    "tv_probe_storage_rewrite", "tv_pool_register", "tv_pool_drain", "tv_mapping_stats",
+    "tv_mapping_release_all",
 )
 
 _lib = None
@@ -99,6 +101,10 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tv_unlink_many": (I, [P, I, I, P]),
         "tv_engine_save_pooled": (I, [P, P, I, P, I, ctypes.c_char_p, P]),
         "tv_recycle_many": (I, [P, I, ctypes.c_char_p, I, P]),
+        "tv_pool_register": (I, [ctypes.c_char_p, I, ctypes.POINTER(L)]),
+        "tv_pool_drain": (I, [ctypes.c_char_p, ctypes.POINTER(L)]),
+        "tv_mapping_stats": (I, [ctypes.POINTER(L), ctypes.POINTER(L)]),
+        "tv_mapping_release_all": (I, []),
         "tv_probe_storage_rewrite": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D),
                                          ctypes.POINTER(D)]),
         "tv_probe_storage_dma": (I, [ctypes.c_char_p, I, L, L, I, ctypes.POINTER(D), ctypes.POINTER(D),
@@ -222,7 +228,8 @@ def write_table(src_base, src_shape, src_off, ext, itemsize, file, device, file_
 # Process-wide counters of native work (bench.py reports the kernel launches and DMA
 # transfers its timed region issued).
 _FIELDS = ("kernel_launches", "dma_copies", "bytes_device", "bytes_storage", "bytes_packed", "files",
-           "seconds_total", "seconds_io", "seconds_wait_dma", "seconds_wait_slot", "recycled_files")
+           "seconds_total", "seconds_io", "seconds_wait_dma", "seconds_wait_slot", "recycled_files",
+           "zero_copy_bytes")
 TOTALS = {"save": dict.fromkeys(_FIELDS, 0), "load": dict.fromkeys(_FIELDS, 0),
           "kernels": {"kernel_launches": 0}, "peer": {"bytes": 0}}
 _totals_lock = threading.Lock()
@@ -325,6 +332,27 @@ def recycle_many(paths: Sequence[str], pool_dir: str, threads: int) -> list[bool
     check(lib().tv_recycle_many(table.pointers.ctypes.data, len(paths), pool_dir.encode(), int(threads),
                                 ok.ctypes.data), "tv_recycle_many")
     return [bool(x) for x in ok]
+
+
+def pool_register(pool_dir: str, threads: int = 4) -> int:
+    """Map + register (CUDA) every not-yet-registered recycle-pool file on a RAM-backed
+    filesystem; bytes registered now (0 without a GPU)."""
+    n = ctypes.c_int64()
+    check(lib().tv_pool_register(pool_dir.encode(), int(threads), ctypes.byref(n)), "tv_pool_register")
+    return n.value
+
+
+def pool_drain(pool_dir: str) -> int:
+    """Release the registrations of, and unlink, every pool file; bytes freed."""
+    n = ctypes.c_int64()
+    check(lib().tv_pool_drain(pool_dir.encode(), ctypes.byref(n)), "tv_pool_drain")
+    return n.value
+
+
+def mapping_stats() -> tuple[int, int]:
+    files, nbytes = ctypes.c_int64(), ctypes.c_int64()
+    check(lib().tv_mapping_stats(ctypes.byref(files), ctypes.byref(nbytes)), "tv_mapping_stats")
+    return files.value, nbytes.value
 
 
 def probe_storage(directory: str, threads: int, file_bytes: int, block_bytes: int) -> tuple[float, float]:

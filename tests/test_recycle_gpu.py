@@ -20,8 +20,23 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-@pytest.mark.parametrize("name", ["fsdp4_per_leaf", "fsdp4_aggregated", "c1_per_leaf"])
-def test_save_over_recycled_files_is_byte_identical(name, tmp_path):
+@pytest.fixture
+def shm_dir(tmp_path):
+    """A directory on a RAM-backed filesystem (the zero-copy half needs tmpfs)."""
+    import shutil
+    import uuid
+
+    from paper_2605_23066_b200 import native
+
+    d = f"/dev/shm/tv_recycle_{uuid.uuid4().hex[:8]}"
+    yield d
+    native.lib().tv_mapping_release_all()  # registrations of this test's files
+    shutil.rmtree(d, ignore_errors=True)
+
+
+@pytest.mark.parametrize("register", [True, False])
+@pytest.mark.parametrize("name", ["fsdp4_per_leaf", "fsdp4_aggregated", "c1_per_leaf", "replica_parallel"])
+def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir):
     import paper_2605_23066_b200 as tv
     from paper_2605_23066_b200 import native
     from paper_2605_23066_b200.training_manager import delete_checkpoint
@@ -31,7 +46,7 @@ def test_save_over_recycled_files_is_byte_identical(name, tmp_path):
         pytest.skip("recycling is a filesystem-backend feature")
     gold = json.loads((GOLDEN / f"{name}.json").read_text())
     tree, specs = cases.build_inputs(c)
-    backend = tv.FilesystemBackend(str(tmp_path))
+    backend = tv.FilesystemBackend(shm_dir, register_pool=register)
     rt = tv.SimulatedRuntime(c["process_count"], backend)
     cps = helpers.checkpointables(tree, specs, rt)
     sh = helpers.shardings_for(tree, specs)
@@ -41,23 +56,52 @@ def test_save_over_recycled_files_is_byte_identical(name, tmp_path):
     delete_checkpoint(backend.store(), "ckpt/old", recycle=True)
     pooled = backend.recycle_pool_bytes()
     assert pooled > 0
-    before = native.totals()["save"]["recycled_files"]
+    before = native.totals()
     tv.save_checkpoint(rt, "ckpt/run", cps, sh, opts).wait()
-    assert native.totals()["save"]["recycled_files"] > before
+    after = native.totals()
+    assert after["save"]["recycled_files"] > before["save"]["recycled_files"]
+    # registered pool: the chunk bytes went straight into the recycled files' pages
+    zero_copy = after["save"]["zero_copy_bytes"] - before["save"]["zero_copy_bytes"]
+    assert (zero_copy > 0) == register
     assert backend.recycle_pool_bytes() == 0  # every retired file was claimed
     got = helpers.dump_digests(backend)
+    got = {k: v for k, v in got.items() if not k.startswith(".tvpool")}
     assert sorted(got) == sorted(gold["files"])
     for key, rec in gold["files"].items():
         assert got[key] == (rec["size"], rec["sha256"]), key
+    # and a restore of it (zero-copy H2D out of the registered pages) is exact
+    before = native.totals()
+    abstracts, mesh, P = helpers.abstracts_for(c, {"mesh": "saved"}, tree, specs)
+    out = tv.load_checkpoint(tv.SimulatedRuntime(P, backend), "ckpt/run", abstracts, tv.LoadOptions(),
+                             current_mesh=mesh)
+    if register:
+        assert native.totals()["load"]["zero_copy_bytes"] > before["load"]["zero_copy_bytes"]
+    for name_cp, value in tree.items():
+        if not isinstance(value, dict):
+            continue
+        for path, leaf in cases.leaf_paths(value):
+            if leaf[0] != "array":
+                continue
+            got_leaf = helpers.get_path(out[name_cp], path)
+            if isinstance(got_leaf, tv.ShardedArray):
+                import treevault_oracle as orc
+
+                m = got_leaf.sharding.mesh
+                spec = orc.Spec(orc.Mesh(list(zip(m.axis_names, m.axis_sizes)), m.process_count,
+                                         m.replica_axis), got_leaf.sharding.spec.entries, leaf[2].shape)
+                assert helpers.leaf_bytes_by_device(got_leaf) == orc.expected_shards(leaf[2], spec), path
+            else:
+                assert got_leaf.tobytes() == leaf[2].tobytes(), path
 
 
-def test_checkpointer_recycle_loop(tmp_path):
+def test_checkpointer_recycle_loop(shm_dir):
     import numpy as np
     import torch
 
     import paper_2605_23066_b200 as tv
+    from paper_2605_23066_b200 import native
 
-    backend = tv.FilesystemBackend(str(tmp_path))
+    backend = tv.FilesystemBackend(shm_dir)
     rt = tv.SimulatedRuntime(2, backend, gpus=[0])
     mesh = tv.Mesh.create([("fsdp", 2)], process_count=2)
     s = tv.Sharding(mesh, tv.PartitionSpec(("fsdp", None)), (256, 128))
@@ -72,6 +116,7 @@ def test_checkpointer_recycle_loop(tmp_path):
     ck.close()  # joins the save and the background retention, drains the pool
     assert ck.all_steps() == [4, 5]
     assert backend.recycle_pool() is None
+    assert native.totals()["save"]["zero_copy_bytes"] > 0
     for step in (4, 5):
         out = ck.load_step(step, options=tv.LoadOptions(to_host=True), current_mesh=mesh)
         assert np.all(out["m"]["w"].data == float(step))
