@@ -180,10 +180,14 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
  * an output of N bytes claims a retired file `<pool_dir>/<N>/<name>` (rename to its
  * `.partial`) and overwrites it in place — no page allocation or zeroing for storage
  * that keeps its pages (tmpfs).  Steady-state checkpointing with retention
- * (training_manager.py:262-295: a step is retired while the next is saved). */
+ * (training_manager.py:262-295: a step is retired while the next is saved).
+ * pool_flags & TV_POOL_REGISTER: a claimed file on a RAM-backed filesystem is mapped and
+ * registered with CUDA (once per file lifetime; cached by inode) and its contiguous items
+ * are DMA'd straight into its page-cache pages (zero-copy). */
+#define TV_POOL_REGISTER 1
 int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
                           const tv_output* outputs, int n_outputs, const char* pool_dir,
-                          tv_stats* stats);
+                          int pool_flags, tv_stats* stats);
 
 /* Restore: fetch every item once, land it on its reader GPU, run its copies
  * (ChunkReader.read_range, chunkstore.py:507-593, _execute_reads + _assemble,

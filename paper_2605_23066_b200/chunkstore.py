@@ -22,6 +22,7 @@ import bisect
 import functools
 import itertools
 import math
+import re
 from bisect import bisect_left
 from dataclasses import dataclass, field
 from typing import Any, Iterable, Iterator, Optional, Sequence
@@ -564,6 +565,15 @@ class ProcessArrayWriter:
         return doc
 
 
+_PROCESS_DIR = re.compile(r"(?:^|/)process_(\d+)/")
+
+
+def process_of_key(key: str) -> int | None:
+    """The logical process whose ``process_<p>/`` directory holds ``key`` (None if none)."""
+    m = _PROCESS_DIR.search(key)
+    return int(m.group(1)) if m else None
+
+
 def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, concurrent: int = 1):
     """Run planned chunk writes through the native engine.
 
@@ -612,9 +622,9 @@ def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, 
                 buf = np.empty(size, np.uint8)
                 host_bufs.append(buf)
                 outputs[i]["host"] = buf.ctypes.data if size else 0
-        pool = backend.recycle_pool() if root is not None else None
+        pool = backend.recycle_pool(process_of_key(out_keys[0])) if root is not None else None
         with native.engine_lease(cfg, concurrent) as eng:
-            stats = eng.save(items, outputs, pool)
+            stats = eng.save(items, outputs, pool, register=bool(getattr(backend, "register_pool", False)))
         if root is not None:
             backend.record_bulk(store.identity, "put", out_keys, [0] * len(out_keys), sizes)
         else:

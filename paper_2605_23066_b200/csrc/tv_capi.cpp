@@ -26,7 +26,8 @@ const std::string& get_error() { return g_last_error; }
 
 int engine_create(int, int64_t, int64_t, int, tv_engine**);
 int engine_destroy(tv_engine*);
-int engine_save(tv_engine*, const tv_write_item*, int, const tv_output*, int, const char*, tv_stats*);
+int engine_save(tv_engine*, const tv_write_item*, int, const tv_output*, int, const char*, int,
+                tv_stats*);
 int engine_load(tv_engine*, const tv_read_item*, int, const tv_input*, int, const tv_copy*, int,
                 tv_stats*);
 int copy_boxes(int, const tv_copy*, int, cudaStream_t);
@@ -96,19 +97,19 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
     tv::set_error("tv_engine_save: bad arguments");
     return TV_ERR_ARG;
   }
-  return tv::engine_save(e, items, n_items, outputs, n_outputs, nullptr, stats);
+  return tv::engine_save(e, items, n_items, outputs, n_outputs, nullptr, 0, stats);
 }
 
 int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
                           const tv_output* outputs, int n_outputs, const char* pool_dir,
-                          tv_stats* stats) {
+                          int pool_flags, tv_stats* stats) {
   tv::DeviceGuard guard;
   if (!e || n_items < 0 || n_outputs < 0) {
     tv::set_error("tv_engine_save_pooled: bad arguments");
     return TV_ERR_ARG;
   }
   return tv::engine_save(e, items, n_items, outputs, n_outputs,
-                         (pool_dir && pool_dir[0]) ? pool_dir : nullptr, stats);
+                         (pool_dir && pool_dir[0]) ? pool_dir : nullptr, pool_flags, stats);
 }
 
 int tv_engine_load(tv_engine* e, const tv_read_item* items, int n_items, const tv_input* inputs,

@@ -615,9 +615,9 @@ class FilePool {
 class SaveRun {
  public:
   SaveRun(tv_engine* e, const tv_write_item* items, int n_items, const tv_output* outs,
-          int n_outs, tv_stats* st, const char* pool_dir = nullptr)
+          int n_outs, tv_stats* st, const char* pool_dir = nullptr, int pool_flags = 0)
       : e_(e), items_(items), n_items_(n_items), n_outs_(n_outs), stats_(st),
-        pool_(pool_dir ? pool_dir : "") {
+        pool_(pool_dir ? pool_dir : ""), pool_flags_(pool_flags) {
     outs_.reset(new OutputState[n_outs]);
     for (int i = 0; i < n_outs; ++i) {
       outs_[i].path = outs[i].path ? outs[i].path : "";
@@ -655,7 +655,7 @@ class SaveRun {
     }
     for (int s = 0; s < e_->n_slots; ++s) free_slots_.push(s);
     direct_.assign(n_items_, 0);
-    if (!pool_.empty() && mappings_exist()) claim_outputs();
+    if (!pool_.empty()) claim_outputs();
     assign_lanes();
     std::vector<std::thread> writers;
     for (int t = 0; t < (int)lanes_.size(); ++t) writers.emplace_back([this, t] { writer_loop(t); });
@@ -702,7 +702,11 @@ class SaveRun {
       OutputState& out = outs_[o];
       if (out.path.empty() || out.size == 0) continue;
       std::call_once(out.opened, [&] { open_output(out); });
-      if (out.fd >= 0 && claimed_[o]) out.mapped = mapping_for_fd(out.fd, out.size);
+      if (out.fd < 0 || !claimed_[o]) continue;
+      // a recycled file keeps its registration from earlier generations; the first time
+      // this process claims it, register it (once per file lifetime, TV_POOL_REGISTER)
+      out.mapped = (pool_flags_ & TV_POOL_REGISTER) ? mapping_register_fd(out.fd, out.size)
+                                                    : mapping_for_fd(out.fd, out.size);
     }
     for (int i = 0; i < n_items_; ++i) {
       const auto& it = items_[i];
@@ -1027,7 +1031,7 @@ class SaveRun {
     }
     std::string tmp = o.path + ".partial";
     if (!pool_.empty() && o.size > 0 && pool_.claim(o.size, tmp)) {
-      o.fd = ::open(tmp.c_str(), O_WRONLY | O_CLOEXEC);
+      o.fd = ::open(tmp.c_str(), O_RDWR | O_CLOEXEC);  // read-write: mmap-able
       if (o.fd >= 0) {
         recycled_ += 1;
         claimed_[&o - outs_.get()] = 1;
@@ -1099,6 +1103,7 @@ class SaveRun {
   int n_outs_;
   tv_stats* stats_;
   FilePool pool_;
+  const int pool_flags_;
   std::atomic<int64_t> recycled_{0}, zero_copy_bytes_{0};
   std::vector<char> claimed_;                      // output claimed a recycled file
   std::vector<char> direct_;                       // item DMA'd straight into its mapping
@@ -1521,10 +1526,10 @@ int engine_destroy(tv_engine* e) {
 }
 
 int engine_save(tv_engine* e, const tv_write_item* items, int n_items, const tv_output* outputs,
-                int n_outputs, const char* pool_dir, tv_stats* stats) {
+                int n_outputs, const char* pool_dir, int pool_flags, tv_stats* stats) {
   std::lock_guard<std::mutex> g(e->call_m);
   tv_stats local{};
-  SaveRun run(e, items, n_items, outputs, n_outputs, stats ? stats : &local, pool_dir);
+  SaveRun run(e, items, n_items, outputs, n_outputs, stats ? stats : &local, pool_dir, pool_flags);
   int rc = run.run();
   run.publish_stats();
   return rc;

@@ -173,6 +173,26 @@ std::vector<std::string> pool_files(const std::string& pool) {
 
 }  // namespace
 
+char* mapping_register_fd(int fd, int64_t size) {
+  struct stat st;
+  if (fd < 0 || ::fstat(fd, &st) != 0 || !S_ISREG(st.st_mode) || st.st_size != size || size <= 0 ||
+      !ram_backed(fd))
+    return nullptr;
+  if (char* hit = MappingCache::get().find(st.st_dev, st.st_ino, size)) return hit;
+  void* addr = ::mmap(nullptr, (size_t)size, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  if (addr == MAP_FAILED) return nullptr;
+  if (cudaHostRegister(addr, (size_t)size, cudaHostRegisterPortable) != cudaSuccess) {
+    cudaGetLastError();
+    ::munmap(addr, (size_t)size);
+    return nullptr;
+  }
+  Mapping m;
+  m.addr = static_cast<char*>(addr);
+  m.size = size;
+  MappingCache::get().insert(st.st_dev, st.st_ino, m);
+  return m.addr;
+}
+
 char* mapping_for_fd(int fd, int64_t size) {
   if (fd < 0 || MappingCache::get().empty()) return nullptr;
   struct stat st;

@@ -27,6 +27,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libtvgpu.so"
 
 TV_OK = 0
 TV_ERR_IO = -2  # include/tvgpu.h
+POOL_REGISTER = 1  # TV_POOL_REGISTER
 
 # ---- C struct layouts -------------------------------------------------------------------
 
@@ -99,7 +100,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tv_probe_storage": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "tv_probe_pcie": (I, [I, L, I, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "tv_unlink_many": (I, [P, I, I, P]),
-        "tv_engine_save_pooled": (I, [P, P, I, P, I, ctypes.c_char_p, P]),
+        "tv_engine_save_pooled": (I, [P, P, I, P, I, ctypes.c_char_p, I, P]),
         "tv_recycle_many": (I, [P, I, ctypes.c_char_p, I, P]),
         "tv_pool_register": (I, [ctypes.c_char_p, I, ctypes.POINTER(L)]),
         "tv_pool_drain": (I, [ctypes.c_char_p, ctypes.POINTER(L)]),
@@ -427,15 +428,19 @@ class Engine:
             lib().tv_engine_destroy(self._h)
             self._h = None
 
-    def save(self, items: np.ndarray, outputs: np.ndarray, pool_dir: str | None = None) -> np.ndarray:
+    def save(self, items: np.ndarray, outputs: np.ndarray, pool_dir: str | None = None,
+             register: bool = False) -> np.ndarray:
         """Write every item into its output; with ``pool_dir`` outputs reuse recycled
-        files of their exact size (see tv_engine_save_pooled)."""
+        files of their exact size, and with ``register`` DMA straight into their
+        registered page-cache pages (see tv_engine_save_pooled)."""
         stats = np.zeros(1, STATS)
         items = np.ascontiguousarray(items, WRITE_ITEM)
         outputs = np.ascontiguousarray(outputs, OUTPUT)
+        flags = POOL_REGISTER if register else 0
         with _bound_to(self.cpus):
             rc = lib().tv_engine_save_pooled(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
-                                             pool_dir.encode() if pool_dir else None, stats.ctypes.data)
+                                             pool_dir.encode() if pool_dir else None, flags,
+                                             stats.ctypes.data)
         _account("save", stats[0])
         check(rc, "tv_engine_save")
         return stats[0]

@@ -30,8 +30,9 @@ def test_recycle_retires_payloads_and_hides_the_pool(tmp_path):
     assert backend.recycle_pool() is None
     delete_checkpoint(store, "run/step_00000001", recycle=True)
     assert store.list_keys("") == []
-    pool = backend.recycle_pool()
-    assert pool is not None and os.path.basename(pool) == ".tvpool"
+    pool = backend.recycle_pool(0)  # files of process_0 go to its own sub-pool
+    assert pool is not None and pool.endswith(os.path.join(".tvpool", "p0"))
+    assert backend.recycle_pool(1) is None
     sizes = sorted((d, len(os.listdir(os.path.join(pool, d)))) for d in os.listdir(pool))
     assert sizes == [("1000", 1), ("4096", 2)]  # payload files only, grouped by size
     assert backend.recycle_pool_bytes() == 2 * 4096 + 1000
@@ -39,7 +40,7 @@ def test_recycle_retires_payloads_and_hides_the_pool(tmp_path):
     with pytest.raises(BackendError):
         store.put(".tvpool/x", b"1")
     assert backend.drain_recycle_pool() == 2 * 4096 + 1000
-    assert backend.recycle_pool() is None
+    assert backend.recycle_pool(0) is None
 
 
 def test_plain_delete_frees(tmp_path):
@@ -47,7 +48,7 @@ def test_plain_delete_frees(tmp_path):
     store = backend.store()
     _checkpoint(store, "ck")
     delete_checkpoint(store, "ck")
-    assert backend.recycle_pool() is None and store.list_keys("") == []
+    assert backend.recycle_pool(0) is None and store.list_keys("") == []
 
 
 def test_memory_backend_ignores_recycle():
@@ -55,4 +56,4 @@ def test_memory_backend_ignores_recycle():
     store = backend.store()
     _checkpoint(store, "ck")
     delete_checkpoint(store, "ck", recycle=True)
-    assert store.list_keys("") == [] and backend.recycle_pool() is None
+    assert store.list_keys("") == [] and backend.recycle_pool(0) is None

@@ -115,7 +115,7 @@ def test_checkpointer_recycle_loop(shm_dir):
         ck.save_step(step, {"m": {"w": leaf}}, {"m": {"w": s}})
     ck.close()  # joins the save and the background retention, drains the pool
     assert ck.all_steps() == [4, 5]
-    assert backend.recycle_pool() is None
+    assert backend.recycle_pool(0) is None and backend.recycle_pool(1) is None
     assert native.totals()["save"]["zero_copy_bytes"] > 0
     for step in (4, 5):
         out = ck.load_step(step, options=tv.LoadOptions(to_host=True), current_mesh=mesh)
