@@ -662,12 +662,27 @@ class SaveRun {
     // Zero-byte outputs are committed up front.
     for (int o = 0; o < n_outs_; ++o)
       if (outs_[o].size == 0) finish_output(o);
-    std::thread finisher;
-    if (!err_.failed.load() && issue_direct()) finisher = std::thread([this] { finish_direct(); });
+    std::thread zero_copy;
+    if (!zq_.empty()) zero_copy = std::thread([this] { zero_copy_loop(); });
     produce();
+    if (steal_) {
+      // the slot path takes zero-copy items from the back of the queue while the DMA
+      // path takes them from the front: the two paths split the work at their own rates
+      while (!err_.failed.load()) {
+        std::vector<int> batch;
+        for (int k = 0; k < std::max(1, e_->n_threads); ++k) {
+          int i;
+          if (!take_back(&i)) break;
+          batch.push_back(i);
+        }
+        if (batch.empty()) break;
+        for (int i : batch) cursors_[lane_of_[items_[i].file]].items.push_back(i);
+        produce();
+      }
+    }
     for (auto& q : lanes_) q->close();
     for (auto& w : writers) w.join();
-    if (finisher.joinable()) finisher.join();
+    if (zero_copy.joinable()) zero_copy.join();
     for (auto& ev : events_) cudaEventDestroy(ev);
     if (err_.failed.load()) {
       abort_outputs();
@@ -712,68 +727,101 @@ class SaveRun {
       const auto& it = items_[i];
       const int64_t n = box_bytes(it.ext, it.rank, it.itemsize);
       int64_t boff = 0, bn = 0;
-      if (n > 0 && outs_[it.file].mapped && box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn))
+      if (n > 0 && outs_[it.file].mapped && box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn)) {
         direct_[i] = 1;
+        zq_.push_back(i);
+      }
     }
+    zhi_ = zq_.size();
+    const char* v = std::getenv("TVGPU_SAVE_STEAL");
+    steal_ = v ? std::atoi(v) != 0 : false;
   }
 
-  // D2H of every direct item on its device's zero-copy stream; one event per device.
-  bool issue_direct() {
-    std::map<int, cudaStream_t> used;
-    for (int i = 0; i < n_items_; ++i) {
-      if (!direct_[i]) continue;
+  bool take_front(int* i) {
+    std::lock_guard<std::mutex> g(zq_m_);
+    if (zlo_ >= zhi_) return false;
+    *i = zq_[zlo_++];
+    return true;
+  }
+  bool take_back(int* i) {
+    std::lock_guard<std::mutex> g(zq_m_);
+    if (zlo_ >= zhi_) return false;
+    *i = zq_[--zhi_];
+    return true;
+  }
+
+  // The DMA path: zero-copy items from the front of the queue, D2H straight into the
+  // registered pages of their output on the device's zero-copy stream, at most `window`
+  // bytes in flight; an item's bytes count toward its output once its event completed.
+  void zero_copy_loop() {
+    const char* w = std::getenv("TVGPU_ZC_WINDOW");
+    const int64_t window = w ? std::atoll(w) : (int64_t)1 << 30;
+    struct Flight {
+      int item;
+      int device;
+      int64_t n;
+      cudaEvent_t ev;
+    };
+    std::deque<Flight> flight;
+    int64_t in_flight = 0;
+    auto retire = [&](const Flight& f) {
+      cudaSetDevice(f.device);
+      const double t0 = now_s();
+      cudaError_t ce = cudaEventSynchronize(f.ev);
+      wait_dma_.add(now_s() - t0);
+      cudaEventDestroy(f.ev);
+      if (ce != cudaSuccess) {
+        err_.set(TV_ERR_CUDA, std::string("zero-copy D2H: ") + cudaGetErrorString(ce));
+        return false;
+      }
+      stats_bytes_storage_ += f.n;
+      zero_copy_bytes_ += f.n;
+      OutputState& o = outs_[items_[f.item].file];
+      if (o.left.fetch_sub(f.n) == f.n) return finish_output(items_[f.item].file);
+      return true;
+    };
+    int i;
+    while (!err_.failed.load() && take_front(&i)) {
       const auto& it = items_[i];
       DeviceCtx* ctx = nullptr;
       int rc = device_ctx(e_, it.device, &ctx);
       if (rc != TV_OK) {
         err_.set(rc, get_error());
-        return false;
+        break;
       }
       cudaSetDevice(it.device);
       int64_t boff = 0, bn = 0;
       box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn);
       const char* src = reinterpret_cast<const char*>(it.src.base) + boff;
-      OutputState& o = outs_[it.file];
-      if (cudaMemcpyAsync(o.mapped + it.file_off, src, bn, cudaMemcpyDefault, ctx->zero_copy) !=
-          cudaSuccess) {
+      cudaEvent_t ev;
+      if (cudaMemcpyAsync(outs_[it.file].mapped + it.file_off, src, bn, cudaMemcpyDefault,
+                          ctx->zero_copy) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventRecord(ev, ctx->zero_copy) != cudaSuccess) {
         err_.set(TV_ERR_CUDA, std::string("zero-copy D2H: ") + cudaGetErrorString(cudaGetLastError()));
-        return false;
+        break;
       }
-      o.direct += bn;
-      used[it.device] = ctx->zero_copy;
       stats_dma_ += 1;
       stats_bytes_device_ += bn;
-    }
-    for (auto& kv : used) {
-      cudaSetDevice(kv.first);
-      cudaEvent_t ev;
-      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventRecord(ev, kv.second) != cudaSuccess) {
-        err_.set(TV_ERR_CUDA, "zero-copy event");
-        return false;
+      flight.push_back({i, it.device, bn, ev});
+      in_flight += bn;
+      while (in_flight > window && !flight.empty()) {
+        Flight f = flight.front();
+        flight.pop_front();
+        in_flight -= f.n;
+        if (!retire(f)) break;
       }
-      direct_events_.push_back({kv.first, ev});
     }
-    return !direct_events_.empty();
-  }
-
-  // When the direct DMAs have landed: count their bytes; outputs complete -> commit.
-  void finish_direct() {
-    for (auto& de : direct_events_) {
-      cudaSetDevice(de.first);
-      const double t0 = now_s();
-      cudaError_t ce = cudaEventSynchronize(de.second);
-      wait_dma_.add(now_s() - t0);
-      cudaEventDestroy(de.second);
-      if (ce != cudaSuccess) err_.set(TV_ERR_CUDA, std::string("zero-copy D2H: ") + cudaGetErrorString(ce));
-    }
-    if (err_.failed.load()) return;
-    for (int o = 0; o < n_outs_; ++o) {
-      OutputState& out = outs_[o];
-      if (!out.mapped || out.direct == 0) continue;
-      stats_bytes_storage_ += out.direct;
-      zero_copy_bytes_ += out.direct;
-      if (out.left.fetch_sub(out.direct) == out.direct && !finish_output(o)) return;
+    while (!flight.empty()) {  // drain (also after an error: no event is left behind)
+      Flight f = flight.front();
+      flight.pop_front();
+      if (err_.failed.load()) {
+        cudaSetDevice(f.device);
+        cudaEventSynchronize(f.ev);
+        cudaEventDestroy(f.ev);
+        continue;
+      }
+      retire(f);
     }
   }
 
@@ -1106,8 +1154,11 @@ class SaveRun {
   const int pool_flags_;
   std::atomic<int64_t> recycled_{0}, zero_copy_bytes_{0};
   std::vector<char> claimed_;                      // output claimed a recycled file
-  std::vector<char> direct_;                       // item DMA'd straight into its mapping
-  std::vector<std::pair<int, cudaEvent_t>> direct_events_;
+  std::vector<char> direct_;                       // item eligible for the zero-copy path
+  std::vector<int> zq_;                            // zero-copy queue (item order)
+  std::mutex zq_m_;
+  size_t zlo_ = 0, zhi_ = 0;                       // front (DMA path) / back (slot path)
+  bool steal_ = false;                             // TVGPU_SAVE_STEAL: slot path steals from the back
   std::unique_ptr<OutputState[]> outs_;
   Queue<int> free_slots_;
   std::vector<std::unique_ptr<Queue<SaveSlot>>> lanes_;
