@@ -751,12 +751,15 @@ def run_ours(args) -> dict:
         "restore_ms": round(restore_ms, 2),
         "retire_ms": round(retire_ms, 2),
         "recycle": {"enabled": bool(args.recycle),
+                    "save_path_rates_rank0": native.SAVE_PATHS.snapshot(),
                     "files_overwritten_in_timed_steps": int(d.sum(after["save"]["recycled_files"]
                                                                   - before["save"]["recycled_files"])),
                     "note": "each step ends by retiring its checkpoint (process 0, inside the timed step); "
                             "with recycling its chunk files go to the backend's recycle pool and the next "
                             "save overwrites them in place (FilesystemBackend .tvpool; steady-state "
-                            "checkpointing with max_to_keep) instead of allocating fresh page-cache pages"},
+                            "checkpointing with max_to_keep) instead of allocating fresh page-cache pages; "
+                            "each GPU's saves use whichever of zero-copy (D2H into the registered pages) and "
+                            "slot ring + pwrite measured faster on this box (native.SavePathChooser)"},
         "wall_ms_per_step": round(statistics.mean(walls), 2),
         "save_mode": args.save_mode,
         "async_blocking_ms": round(blocking_ms + snap_dev_ms, 2),
@@ -951,6 +954,11 @@ def c5_loop(tv, d, rt, N: int, base: str, layers: int, steps: int, train_ms: flo
     steady = total[1:] or total  # the first save_step also warms plan caches
     host_steady = blocking[1:] or blocking
     mean = statistics.mean(steady)
+    # recycling steady state: step k reuses step k-4's files (keep_last=3 + the save in
+    # flight), and a file is CUDA-registered the first time its process claims it, so
+    # from step 8 every save overwrites registered files
+    warm = 2 * (3 + 1)
+    recycled = total[warm:]
     del state, params
     d.barrier()
     if d.rank == 0:
@@ -976,6 +984,11 @@ def c5_loop(tv, d, rt, N: int, base: str, layers: int, steps: int, train_ms: flo
         "sync_save_ms": round(sync_save_ms, 2),
         "blocking_frac_of_sync_save": round(mean / sync_save_ms, 4),
         "blocking_p99_frac_of_sync_save": round(_pct(steady, 99) / sync_save_ms, 4),
+        "steady_state": ({"from_step": warm, "blocking_ms_mean": round(statistics.mean(recycled), 2),
+                          "blocking_ms_p99": round(_pct(recycled, 99), 2),
+                          "frac_of_sync_save": round(statistics.mean(recycled) / sync_save_ms, 4),
+                          "note": "steps whose save overwrites recycled, already-registered files"}
+                         if recycled else None),
         "loop_seconds": round(loop_s, 2),
         "retained_steps": kept,
         "save_phases_ms_mean_rank0": {k: round(v / max(1, steps - 1), 2) for k, v in phase_sums.items()},
@@ -1554,7 +1567,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--e2e-steps", type=int, default=5)

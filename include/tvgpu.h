@@ -183,7 +183,8 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
  * (training_manager.py:262-295: a step is retired while the next is saved).
  * pool_flags & TV_POOL_REGISTER: a claimed file on a RAM-backed filesystem is mapped and
  * registered with CUDA (once per file lifetime; cached by inode) and its contiguous items
- * are DMA'd straight into its page-cache pages (zero-copy). */
+ * are DMA'd straight into its page-cache pages (zero-copy); without it every output takes
+ * the pinned slot + pwrite path. */
 #define TV_POOL_REGISTER 1
 int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
                           const tv_output* outputs, int n_outputs, const char* pool_dir,

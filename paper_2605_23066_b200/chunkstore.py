@@ -623,8 +623,15 @@ def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, 
                 host_bufs.append(buf)
                 outputs[i]["host"] = buf.ctypes.data if size else 0
         pool = backend.recycle_pool(process_of_key(out_keys[0])) if root is not None else None
+        gpu = int(pending[0].region.gpu)
+        zero_copy = bool(pool) and bool(getattr(backend, "register_pool", False)) and native.SAVE_PATHS.choose(gpu)
+        registered_before = native.mapping_stats()[0] if zero_copy else 0
         with native.engine_lease(cfg, concurrent) as eng:
-            stats = eng.save(items, outputs, pool, register=bool(getattr(backend, "register_pool", False)))
+            stats = eng.save(items, outputs, pool, register=zero_copy)
+        if pool and int(stats["recycled_files"]) > 0:
+            warm_up = zero_copy and native.mapping_stats()[0] > registered_before  # registered new files
+            native.SAVE_PATHS.record(gpu, zero_copy, int(stats["bytes_storage"]), float(stats["seconds_total"]),
+                                     warm_up)
         if root is not None:
             backend.record_bulk(store.identity, "put", out_keys, [0] * len(out_keys), sizes)
         else:

@@ -718,10 +718,10 @@ class SaveRun {
       if (out.path.empty() || out.size == 0) continue;
       std::call_once(out.opened, [&] { open_output(out); });
       if (out.fd < 0 || !claimed_[o]) continue;
-      // a recycled file keeps its registration from earlier generations; the first time
-      // this process claims it, register it (once per file lifetime, TV_POOL_REGISTER)
-      out.mapped = (pool_flags_ & TV_POOL_REGISTER) ? mapping_register_fd(out.fd, out.size)
-                                                    : mapping_for_fd(out.fd, out.size);
+      // TV_POOL_REGISTER: zero-copy; a recycled file keeps its registration from earlier
+      // generations, and the first time this process claims it, it is registered (once
+      // per file lifetime).  Without the flag the output takes the slot + pwrite path.
+      if (pool_flags_ & TV_POOL_REGISTER) out.mapped = mapping_register_fd(out.fd, out.size);
     }
     for (int i = 0; i < n_items_; ++i) {
       const auto& it = items_[i];

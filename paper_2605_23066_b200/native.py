@@ -356,6 +356,57 @@ def mapping_stats() -> tuple[int, int]:
     return files.value, nbytes.value
 
 
+class SavePathChooser:
+    """Per-GPU choice between the two ways a save can move bytes into recycled files:
+    zero-copy (D2H straight into the registered page-cache pages) or the pinned slot ring
+    + pwrite.  Which is faster depends on the box: one GPU alone streams 54 GB/s
+    zero-copy vs 40 through the slots, while on a 4-GPU box whose GPUs share a host-side
+    DMA path the slot ring (DDIO-resident, the CPUs copy into the page cache) wins for
+    saves (profiles/r02_steal*_n4.json).  Each path is tried on recycled files (a
+    zero-copy save that had to register new files is a warm-up and not scored), the
+    faster one is used, and the other is re-tried every ``RETRY`` saves."""
+
+    RETRY = 64
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._state: dict[int, dict] = {}
+
+    def choose(self, key: int) -> bool:
+        """True = zero-copy for this save."""
+        env = os.environ.get("TVGPU_SAVE_PATH", "auto")
+        if env in ("zero_copy", "slots"):
+            return env == "zero_copy"
+        with self._lock:
+            st = self._state.setdefault(key, {"rate": {True: None, False: None}, "n": 0})
+            st["n"] += 1
+            rz, rs = st["rate"][True], st["rate"][False]
+            if rz is None:
+                return True
+            if rs is None:
+                return False
+            best = rz >= rs
+            return (not best) if st["n"] % self.RETRY == 0 else best
+
+    def record(self, key: int, zero_copy: bool, nbytes: int, seconds: float, warm_up: bool) -> None:
+        if warm_up or seconds <= 0 or nbytes <= 0:
+            return
+        with self._lock:
+            st = self._state.setdefault(key, {"rate": {True: None, False: None}, "n": 0})
+            rate = nbytes / seconds
+            old = st["rate"][zero_copy]
+            st["rate"][zero_copy] = rate if old is None else 0.5 * old + 0.5 * rate
+
+    def snapshot(self) -> dict:
+        with self._lock:
+            return {k: {"zero_copy_GBps": None if v["rate"][True] is None else round(v["rate"][True] / 1e9, 2),
+                        "slots_GBps": None if v["rate"][False] is None else round(v["rate"][False] / 1e9, 2)}
+                    for k, v in self._state.items()}
+
+
+SAVE_PATHS = SavePathChooser()
+
+
 def probe_storage(directory: str, threads: int, file_bytes: int, block_bytes: int) -> tuple[float, float]:
     w, r = ctypes.c_double(), ctypes.c_double()
     check(

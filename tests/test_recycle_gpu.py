@@ -36,7 +36,7 @@ def shm_dir(tmp_path):
 
 @pytest.mark.parametrize("register", [True, False])
 @pytest.mark.parametrize("name", ["fsdp4_per_leaf", "fsdp4_aggregated", "c1_per_leaf", "replica_parallel"])
-def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir):
+def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir, monkeypatch):
     import paper_2605_23066_b200 as tv
     from paper_2605_23066_b200 import native
     from paper_2605_23066_b200.training_manager import delete_checkpoint
@@ -46,6 +46,7 @@ def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir):
         pytest.skip("recycling is a filesystem-backend feature")
     gold = json.loads((GOLDEN / f"{name}.json").read_text())
     tree, specs = cases.build_inputs(c)
+    monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")  # (register=False: no zero-copy at all)
     backend = tv.FilesystemBackend(shm_dir, register_pool=register)
     rt = tv.SimulatedRuntime(c["process_count"], backend)
     cps = helpers.checkpointables(tree, specs, rt)
@@ -94,13 +95,14 @@ def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir):
                 assert got_leaf.tobytes() == leaf[2].tobytes(), path
 
 
-def test_checkpointer_recycle_loop(shm_dir):
+def test_checkpointer_recycle_loop(shm_dir, monkeypatch):
     import numpy as np
     import torch
 
     import paper_2605_23066_b200 as tv
     from paper_2605_23066_b200 import native
 
+    monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")
     backend = tv.FilesystemBackend(shm_dir)
     rt = tv.SimulatedRuntime(2, backend, gpus=[0])
     mesh = tv.Mesh.create([("fsdp", 2)], process_count=2)
@@ -120,3 +122,31 @@ def test_checkpointer_recycle_loop(shm_dir):
     for step in (4, 5):
         out = ck.load_step(step, options=tv.LoadOptions(to_host=True), current_mesh=mesh)
         assert np.all(out["m"]["w"].data == float(step))
+
+
+@pytest.mark.parametrize("path", ["zero_copy", "slots"])
+def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
+    """The adaptive save-path choice may pick either path for a recycled save: both
+    write the reference's bytes."""
+    import paper_2605_23066_b200 as tv
+    from paper_2605_23066_b200 import native
+    from paper_2605_23066_b200.training_manager import delete_checkpoint
+
+    monkeypatch.setenv("TVGPU_SAVE_PATH", path)
+    c = cases.case("fsdp4_per_leaf")
+    gold = json.loads((GOLDEN / "fsdp4_per_leaf.json").read_text())
+    tree, specs = cases.build_inputs(c)
+    backend = tv.FilesystemBackend(shm_dir)
+    rt = tv.SimulatedRuntime(c["process_count"], backend)
+    cps = helpers.checkpointables(tree, specs, rt)
+    sh = helpers.shardings_for(tree, specs)
+    for i in range(3):  # fresh, then over recycled (registered on first claim), then again
+        before = native.totals()["save"]
+        tv.save_checkpoint(rt, "ckpt/run", cps, sh, tv.SaveOptions(**c["options"])).wait()
+        after = native.totals()["save"]
+        got = {k: v for k, v in helpers.dump_digests(backend).items() if not k.startswith(".tvpool")}
+        assert got == {k: (r["size"], r["sha256"]) for k, r in gold["files"].items()}
+        if i > 0:
+            zc = after["zero_copy_bytes"] - before["zero_copy_bytes"]
+            assert (zc > 0) == (path == "zero_copy")
+        delete_checkpoint(backend.store(), "ckpt/run", recycle=True)
