@@ -1114,7 +1114,7 @@ def merge_process_indices(store: Store, ckpt_prefix: str, process_count: int) ->
             raw = store.get(f"{pdir}/{ARRAY_METADATA_FILE}")
         except MissingKeyError:
             raise ConsistencyError(f"missing array metadata for process {p}") from None
-        doc = docio.loads(raw, what=f"process {p} array metadata")
+        doc = docio.loads_fast(raw, what=f"process {p} array metadata")
         if layout is None:
             layout = doc.get("layout")
         elif doc.get("layout") != layout:
@@ -1129,25 +1129,30 @@ def merge_process_indices(store: Store, ckpt_prefix: str, process_count: int) ->
         entries = doc.get("arrays", {})
         leaf_sets.append(set(entries))
         for leaf, entry in entries.items():
-            meta = ArrayStorageMetadata.from_json(entry)
-            if leaf not in metas:
+            known = arrays.get(leaf)
+            if known is None:
+                meta = ArrayStorageMetadata.from_json(entry)
                 metas[leaf] = meta
-                arrays[leaf] = {**meta.to_json(), "sharding": entry.get("sharding"), "chunks": {}}
-            elif metas[leaf] != meta:
+                arrays[leaf] = known = {**meta.to_json(), "sharding": entry.get("sharding"), "chunks": {}}
+            elif (entry.get("global_shape") != known["global_shape"] or entry.get("dtype") != known["dtype"]
+                  or entry.get("shard_shape") != known["shard_shape"]
+                  or entry.get("write_chunk") != known["write_chunk"]
+                  or entry.get("read_chunk") != known["read_chunk"] or entry.get("layout") != known["layout"]):
+                ArrayStorageMetadata.from_json(entry)  # a malformed entry raises CorruptionError
                 raise ConsistencyError(f"process {p} disagrees on storage metadata for {leaf!r}")
-            elif arrays[leaf]["sharding"] != entry.get("sharding"):
+            elif known["sharding"] != entry.get("sharding"):
                 raise ConsistencyError(f"process {p} disagrees on sharding for {leaf!r}")
-            located = arrays[leaf]["chunks"]
+            located = known["chunks"]
             for ck in entry.get("chunks", []):
                 if ck in located:
                     raise DuplicateChunkError(
                         f"chunk {ck} of {leaf!r} claimed by processes {located[ck]['p']} and {p}"
                     )
-                loc: dict = {"p": p}
                 if manifest is not None:
                     fid, off, length = manifest.lookup(f"{leaf}/c.{ck}")
-                    loc.update({"f": fid, "o": off, "l": length})
-                located[ck] = loc
+                    located[ck] = {"p": p, "f": fid, "o": off, "l": length}
+                else:
+                    located[ck] = {"p": p}
     if any(s != set(arrays) for s in leaf_sets):
         raise ConsistencyError("processes disagree on the array leaf set")
     for leaf, entry in arrays.items():
