@@ -713,7 +713,9 @@ def run_ours(args) -> dict:
     kern = kernel_roofline(tv, native, state, rt, d, ksave, kload, args, step_ms, peer_gb)
     reshard = (reshard_leg(tv, native, d, rt, wl, state, shardings, args, N, base)
                if args.reshard_steps > 0 and wl.name == "c2" else None)
+    free_recycle_pool(native, d, backend)  # the main tree's retired files: not needed again
     e2e = end_to_end(tv, rt, wl, args, d, base) if not args.no_e2e else None
+    free_recycle_pool(native, d, backend)
     c5 = None
     if args.c5_layers > 0 and wl.name == "c2":
         # BASELINE configs[4] in the default line: the training loop's blocking time with a
@@ -722,6 +724,7 @@ def run_ours(args) -> dict:
         del state
         torch.cuda.empty_cache()
         c5 = c5_loop(tv, d, rt, N, base, args.c5_layers, args.c5_steps, args.train_ms, recycle=args.recycle)
+        free_recycle_pool(native, d, backend)
 
     peaks = measured_peaks()
     result = {
@@ -1173,6 +1176,17 @@ def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, st
     }
 
 
+def free_recycle_pool(native, d, backend) -> None:
+    """Between bench legs: free the recycle pool (process 0) and every rank's CUDA
+    registrations of its files, so the next leg's tree has the RAM-backed storage."""
+    d.barrier()
+    if d.rank == 0:
+        backend.drain_recycle_pool()
+    d.barrier()
+    native.lib().tv_mapping_release_all()
+    d.barrier()
+
+
 def reshard_leg(tv, native, d, rt, wl, state, shardings, args, N: int, base: str) -> dict:
     """BASELINE's reshard GB/s in the default line: the step's checkpoint (FSDP-N) restored
     onto another sharding of the same GPUs — at N >= 2 the C4 target shape (replica 2 x
@@ -1227,6 +1241,9 @@ def reshard_leg(tv, native, d, rt, wl, state, shardings, args, N: int, base: str
         del out  # (no empty_cache: the next restore reuses the block, peers' mappings stay valid)
     d.barrier()
     if d.rank == 0:
+        from paper_2605_23066_b200.training_manager import delete_checkpoint
+
+        delete_checkpoint(rt.backend.store("retention"), path, recycle=args.recycle)
         shutil.rmtree(os.path.join(base, "bench"), ignore_errors=True)
     ms = statistics.mean(times)
     return {

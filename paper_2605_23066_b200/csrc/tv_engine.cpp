@@ -713,16 +713,35 @@ class SaveRun {
   // registered, every contiguous item of the output is DMA'd straight into them and
   // never touches a pinned slot or a writer thread.
   void claim_outputs() {
-    for (int o = 0; o < n_outs_ && !err_.failed.load(); ++o) {
+    // outputs are claimed by a few threads (rename + open + inode lookup, and the one-time
+    // registration of a file this process has not claimed before)
+    std::atomic<int> next{0};
+    auto work = [&] {
+      for (int o = next.fetch_add(1); o < n_outs_ && !err_.failed.load(); o = next.fetch_add(1))
+        claim_output(o);
+    };
+    const int t = std::max(1, std::min({8, e_->n_threads, n_outs_}));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < t; ++k) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    build_zero_copy_queue();
+  }
+
+  void claim_output(int o) {
+    {
       OutputState& out = outs_[o];
-      if (out.path.empty() || out.size == 0) continue;
+      if (out.path.empty() || out.size == 0) return;
       std::call_once(out.opened, [&] { open_output(out); });
-      if (out.fd < 0 || !claimed_[o]) continue;
+      if (out.fd < 0 || !claimed_[o]) return;
       // TV_POOL_REGISTER: zero-copy; a recycled file keeps its registration from earlier
       // generations, and the first time this process claims it, it is registered (once
       // per file lifetime).  Without the flag the output takes the slot + pwrite path.
       if (pool_flags_ & TV_POOL_REGISTER) out.mapped = mapping_register_fd(out.fd, out.size);
     }
+  }
+
+  void build_zero_copy_queue() {
     for (int i = 0; i < n_items_; ++i) {
       const auto& it = items_[i];
       const int64_t n = box_bytes(it.ext, it.rank, it.itemsize);
