@@ -994,6 +994,8 @@ def c5_loop(tv, d, rt, N: int, base: str, layers: int, steps: int, train_ms: flo
                          if recycled else None),
         "loop_seconds": round(loop_s, 2),
         "retained_steps": kept,
+        "blocking_ms_per_step": [round(x, 2) for x in total],
+        "background_save_ms_per_step": [round(x, 1) for x in bg],
         "save_phases_ms_mean_rank0": {k: round(v / max(1, steps - 1), 2) for k, v in phase_sums.items()},
         "how": "blocking per step = wall time in save_step (max over ranks) + the snapshot kernel's device "
                "time on the training stream (CUDA events, libtvgpu tv_kernel_timing); first step excluded",
@@ -1216,7 +1218,10 @@ def reshard_leg(tv, native, d, rt, wl, state, shardings, args, N: int, base: str
     abstract = {"state": tree}
     # the restored copy lives next to the state: skip (with a note) when HBM cannot hold it
     per_gpu = wl.tree_bytes * (2 if N >= 2 else 1) // max(1, N)
-    free = torch.cuda.mem_get_info(d.local if d.on else 0)[0]
+    dev = d.local if d.on else 0
+    # free HBM plus blocks the caching allocator holds but nothing uses (e.g. the async
+    # snapshot arena of the last save, cached on the caller's stream)
+    free = torch.cuda.mem_get_info(dev)[0] + torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
     if d.max(-free) > -(per_gpu + (4 << 30)):  # min over ranks of free HBM < need
         return {"target": target, "skipped": f"needs {per_gpu / 1e9:.1f} GB of free HBM per GPU next to the "
                                              f"state; have {d.max(-free) * -1 / 1e9:.1f}"}

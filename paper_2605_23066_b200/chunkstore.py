@@ -623,7 +623,8 @@ def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, 
                 host_bufs.append(buf)
                 outputs[i]["host"] = buf.ctypes.data if size else 0
         pool = backend.recycle_pool(process_of_key(out_keys[0])) if root is not None else None
-        gpu = int(pending[0].region.gpu)
+        # per GPU and save size (rates of a 4 GB and an 80 GB save are not comparable)
+        gpu = (int(pending[0].region.gpu), max(1, sum(sizes)).bit_length())
         zero_copy = bool(pool) and bool(getattr(backend, "register_pool", False)) and native.SAVE_PATHS.choose(gpu)
         registered_before = native.mapping_stats()[0] if zero_copy else 0
         with native.engine_lease(cfg, concurrent) as eng:

@@ -370,9 +370,9 @@ class SavePathChooser:
 
     def __init__(self):
         self._lock = threading.Lock()
-        self._state: dict[int, dict] = {}
+        self._state: dict = {}
 
-    def choose(self, key: int) -> bool:
+    def choose(self, key) -> bool:
         """True = zero-copy for this save."""
         env = os.environ.get("TVGPU_SAVE_PATH", "auto")
         if env in ("zero_copy", "slots"):
@@ -388,7 +388,7 @@ class SavePathChooser:
             best = rz >= rs
             return (not best) if st["n"] % self.RETRY == 0 else best
 
-    def record(self, key: int, zero_copy: bool, nbytes: int, seconds: float, warm_up: bool) -> None:
+    def record(self, key, zero_copy: bool, nbytes: int, seconds: float, warm_up: bool) -> None:
         if warm_up or seconds <= 0 or nbytes <= 0:
             return
         with self._lock:
@@ -399,7 +399,7 @@ class SavePathChooser:
 
     def snapshot(self) -> dict:
         with self._lock:
-            return {k: {"zero_copy_GBps": None if v["rate"][True] is None else round(v["rate"][True] / 1e9, 2),
+            return {str(k): {"zero_copy_GBps": None if v["rate"][True] is None else round(v["rate"][True] / 1e9, 2),
                         "slots_GBps": None if v["rate"][False] is None else round(v["rate"][False] / 1e9, 2)}
                     for k, v in self._state.items()}
 
