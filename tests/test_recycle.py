@@ -57,3 +57,31 @@ def test_memory_backend_ignores_recycle():
     _checkpoint(store, "ck")
     delete_checkpoint(store, "ck", recycle=True)
     assert store.list_keys("") == [] and backend.recycle_pool(0) is None
+
+
+def test_process_of_key():
+    from paper_2605_23066_b200.chunkstore import process_of_key
+
+    assert process_of_key("run/step_00000001/process_3/state/w/c.0.0") == 3
+    assert process_of_key("ck/process_12/d/0") == 12
+    assert process_of_key("ck/global_metadata.json") is None
+
+
+def test_save_path_chooser_explores_then_exploits(monkeypatch):
+    from paper_2605_23066_b200.native import SavePathChooser
+
+    monkeypatch.delenv("TVGPU_SAVE_PATH", raising=False)
+    c = SavePathChooser()
+    key = (0, 37)
+    assert c.choose(key) is True                      # explore zero-copy first
+    c.record(key, True, 10 << 30, 1.0, warm_up=True)  # registered new files: not scored
+    assert c.choose(key) is True
+    c.record(key, True, 50 << 30, 1.0, warm_up=False)
+    assert c.choose(key) is False                     # then the slot path
+    c.record(key, False, 30 << 30, 1.0, warm_up=False)
+    picks = [c.choose(key) for _ in range(c.RETRY)]
+    assert picks.count(True) == c.RETRY - 1           # exploit, re-trying the other once
+    other = (1, 37)                                   # another GPU / size: its own estimate
+    assert c.choose(other) is True
+    monkeypatch.setenv("TVGPU_SAVE_PATH", "slots")
+    assert c.choose(key) is False
