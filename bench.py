@@ -725,6 +725,7 @@ def run_ours(args) -> dict:
         torch.cuda.empty_cache()
         c5 = c5_loop(tv, d, rt, N, base, args.c5_layers, args.c5_steps, args.train_ms, recycle=args.recycle)
         free_recycle_pool(native, d, backend)
+    c1 = c1_leg(tv, native, d, base, args) if args.c1_steps > 0 and wl.name == "c2" else None
 
     peaks = measured_peaks()
     result = {
@@ -786,6 +787,7 @@ def run_ours(args) -> dict:
         "roofline": kern,
         "e2e": e2e,
         "c5": c5,
+        "c1": c1,
         "reshard": reshard,
         "gpu_launches": int(kernels),
         "gpu_launches_breakdown": {
@@ -1175,6 +1177,69 @@ def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, st
         "ms_per_launch": round(ms, 3),
         "host_enqueue_ms": round(host_ms, 3),
         "launches_in_timed_region": 0,
+    }
+
+
+def c1_leg(tv, native, d, base: str, args) -> dict | None:
+    """BASELINE configs[0] in the default line: a single-process save + restore round trip
+    of 4 x (4096, 4096) f32 unsharded arrays (268 MB) to the same storage, on process 0's
+    GPU (rank 0 only under torchrun), timed per step like the main step (async save +
+    wait + restore + retire), restored bytes verified."""
+    import torch
+
+    from paper_2605_23066_b200.training_manager import delete_checkpoint
+
+    d.barrier()
+    if d.rank != 0:
+        d.barrier()
+        return None
+    gpu = d.local if d.on else 0
+    sub = os.path.join(base, "c1leg")
+    backend = tv.FilesystemBackend(sub)
+    rt = tv.SimulatedRuntime(1, backend, gpus=[gpu])
+    gen = torch.Generator(device=f"cuda:{gpu}")
+    gen.manual_seed(0)
+    arrays = {f"a{i}": torch.empty((4096, 4096), dtype=torch.float32, device=f"cuda:{gpu}").normal_(generator=gen)
+              for i in range(4)}
+    tree = {"model": {k: tv.DenseArray("f32", v) for k, v in arrays.items()}}
+    nbytes = 4 * 4096 * 4096 * 4
+    times, saves, restores = [], [], []
+    bad = 0
+    for i in range(args.c1_warmup + args.c1_steps):
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        tv.save_checkpoint(rt, f"c1/{i}", tree, None, tv.SaveOptions(sync=args.save_mode == "sync")).wait()
+        e1.record()
+        out = tv.load_checkpoint(rt, f"c1/{i}", None, tv.LoadOptions())
+        e2.record()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        delete_checkpoint(backend.store("retention"), f"c1/{i}", recycle=args.recycle)
+        retire = (time.perf_counter() - t0) * 1e3
+        if i == args.c1_warmup + args.c1_steps - 1:
+            bad = sum(0 if torch.equal(out["model"][k].data.view(torch.int32), v.view(torch.int32)) else 1
+                      for k, v in arrays.items())
+        del out
+        if i >= args.c1_warmup:
+            saves.append(e0.elapsed_time(e1))
+            restores.append(e1.elapsed_time(e2))
+            times.append(e0.elapsed_time(e2) + retire)
+    backend.drain_recycle_pool()
+    shutil.rmtree(sub, ignore_errors=True)
+    d.barrier()
+    ms = statistics.mean(times)
+    return {
+        "workload": "C1 4 x (4096,4096) f32 unsharded (268435456 bytes), one process, "
+                    f"{args.save_mode} save + restore + retire per step",
+        "value": round(2 * nbytes / (ms / 1e3) / 1e9, 3),
+        "unit": "GB/s",
+        "ms_per_step": round(ms, 2),
+        "save_GBps": round(nbytes / (statistics.mean(saves) / 1e3) / 1e9, 3),
+        "restore_GBps": round(nbytes / (statistics.mean(restores) / 1e3) / 1e9, 3),
+        "steps": args.c1_steps,
+        "warmup": args.c1_warmup,
+        "restore_verified": {"bytes_compared": nbytes, "mismatched_arrays": bad},
     }
 
 
@@ -1614,6 +1679,9 @@ def main() -> None:
     ap.add_argument("--c5-layers", type=int, default=8,
                     help="default line: Llama depth of the embedded C5 Checkpointer loop (0 = skip)")
     ap.add_argument("--c5-steps", type=int, default=20)
+    ap.add_argument("--c1-steps", type=int, default=10,
+                    help="default line: C1 (4 x 64 MiB f32, one process) round trips after the C2 legs (0 = skip)")
+    ap.add_argument("--c1-warmup", type=int, default=3)
     ap.add_argument("--reshard-steps", type=int, default=3,
                     help="default line: restores onto another sharding after the timed steps (0 = skip)")
     ap.add_argument("--inline-gc", action="store_true", help="c5: retention deletes inside wait() (reference)")
