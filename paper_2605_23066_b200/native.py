@@ -360,47 +360,62 @@ class SavePathChooser:
     """Per-GPU choice between the two ways a save can move bytes into recycled files:
     zero-copy (D2H straight into the registered page-cache pages) or the pinned slot ring
     + pwrite.  Which is faster depends on the box: one GPU alone streams 54 GB/s
-    zero-copy vs 40 through the slots, while on a 4-GPU box whose GPUs share a host-side
-    DMA path the slot ring (DDIO-resident, the CPUs copy into the page cache) wins for
-    saves (profiles/r02_steal*_n4.json).  Each path is tried on recycled files (a
-    zero-copy save that had to register new files is a warm-up and not scored), the
-    faster one is used, and the other is re-tried every ``RETRY`` saves."""
+    zero-copy vs 40 through the slots, while on some 4-GPU boxes three GPUs sharing a
+    host-side DMA path get only ~21 GB/s each zero-copy
+    (profiles/r02_bench_c2_n4_allzc.json vs r02_bench_c2_n4_4gpu_box.json).
+
+    Keys are (GPU, save-size bucket): rates of a 4 GB and an 80 GB save are not
+    comparable.  A bucket with both rates uses the faster path; a bucket without them
+    follows its GPU's overall verdict when the GPU has one (no exploration on the
+    critical path of, e.g., a Checkpointer loop that starts after a warm-up); otherwise
+    each path is tried once (a zero-copy save that had to register new files is a
+    warm-up and not scored).  A close call (< 25 % apart) is re-tried every ``RETRY``
+    saves."""
 
     RETRY = 64
+    CLOSE = 1.25
 
     def __init__(self):
         self._lock = threading.Lock()
         self._state: dict = {}
+
+    def _entry(self, key) -> dict:
+        return self._state.setdefault(key, {"rate": {True: None, False: None}, "n": 0})
 
     def choose(self, key) -> bool:
         """True = zero-copy for this save."""
         env = os.environ.get("TVGPU_SAVE_PATH", "auto")
         if env in ("zero_copy", "slots"):
             return env == "zero_copy"
+        gpu = key[0] if isinstance(key, tuple) else key
         with self._lock:
-            st = self._state.setdefault(key, {"rate": {True: None, False: None}, "n": 0})
+            st = self._entry(key)
             st["n"] += 1
             rz, rs = st["rate"][True], st["rate"][False]
-            if rz is None:
-                return True
-            if rs is None:
-                return False
-            best = rz >= rs
-            return (not best) if st["n"] % self.RETRY == 0 else best
+            if rz is not None and rs is not None:
+                best = rz >= rs
+                close = max(rz, rs) < self.CLOSE * min(rz, rs)
+                return (not best) if close and st["n"] % self.RETRY == 0 else best
+            g = self._state.get(("gpu", gpu))
+            if g is not None and g["rate"][True] is not None and g["rate"][False] is not None:
+                return g["rate"][True] >= g["rate"][False]
+            return rz is None
 
     def record(self, key, zero_copy: bool, nbytes: int, seconds: float, warm_up: bool) -> None:
         if warm_up or seconds <= 0 or nbytes <= 0:
             return
+        gpu = key[0] if isinstance(key, tuple) else key
+        rate = nbytes / seconds
         with self._lock:
-            st = self._state.setdefault(key, {"rate": {True: None, False: None}, "n": 0})
-            rate = nbytes / seconds
-            old = st["rate"][zero_copy]
-            st["rate"][zero_copy] = rate if old is None else 0.5 * old + 0.5 * rate
+            for k in (key, ("gpu", gpu)):
+                st = self._entry(k)
+                old = st["rate"][zero_copy]
+                st["rate"][zero_copy] = rate if old is None else 0.5 * old + 0.5 * rate
 
     def snapshot(self) -> dict:
         with self._lock:
             return {str(k): {"zero_copy_GBps": None if v["rate"][True] is None else round(v["rate"][True] / 1e9, 2),
-                        "slots_GBps": None if v["rate"][False] is None else round(v["rate"][False] / 1e9, 2)}
+                             "slots_GBps": None if v["rate"][False] is None else round(v["rate"][False] / 1e9, 2)}
                     for k, v in self._state.items()}
 
 
