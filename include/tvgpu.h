@@ -181,10 +181,11 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
  * `.partial`) and overwrites it in place — no page allocation or zeroing for storage
  * that keeps its pages (tmpfs).  Steady-state checkpointing with retention
  * (training_manager.py:262-295: a step is retired while the next is saved).
- * pool_flags & TV_POOL_REGISTER: a claimed file on a RAM-backed filesystem is mapped and
- * registered with CUDA (once per file lifetime; cached by inode) and its contiguous items
- * are DMA'd straight into its page-cache pages (zero-copy); without it every output takes
- * the pinned slot + pwrite path. */
+ * pool_flags & TV_POOL_REGISTER: a claimed file on a RAM-backed filesystem whose pages are
+ * registered with CUDA (cached by inode) gets its contiguous items DMA'd straight into its
+ * page-cache pages (zero-copy); a claimed file not registered yet is written through the
+ * slot path and queued for background registration (once per file lifetime).  Without
+ * the flag every output takes the pinned slot + pwrite path. */
 #define TV_POOL_REGISTER 1
 int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
                           const tv_output* outputs, int n_outputs, const char* pool_dir,
@@ -227,6 +228,9 @@ int tv_pool_drain(const char* pool_dir, int64_t* freed_bytes);
 int tv_mapping_stats(int64_t* files, int64_t* bytes);
 /* Release every registered mapping (the files stay). */
 int tv_mapping_release_all(void);
+/* Wait for the background registrar (files claimed for the first time are registered off
+ * the save's critical path); pending_before = files it still had queued. */
+int tv_mapping_quiesce(int64_t* pending_before);
 
 /* ---- roofline probes (same run as the numbers they bound) ------------------------- */
 /* fio-style sequential write then read of n_threads files of file_bytes each, in

@@ -626,11 +626,12 @@ def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, 
         # per GPU and save size (rates of a 4 GB and an 80 GB save are not comparable)
         gpu = (int(pending[0].region.gpu), max(1, sum(sizes)).bit_length())
         zero_copy = bool(pool) and bool(getattr(backend, "register_pool", False)) and native.SAVE_PATHS.choose(gpu)
-        registered_before = native.mapping_stats()[0] if zero_copy else 0
         with native.engine_lease(cfg, concurrent) as eng:
             stats = eng.save(items, outputs, pool, register=zero_copy)
         if pool and int(stats["recycled_files"]) > 0:
-            warm_up = zero_copy and native.mapping_stats()[0] > registered_before  # registered new files
+            # a zero-copy save that found unregistered files wrote those through the slot
+            # path (they are being registered in the background): a warm-up, not scored
+            warm_up = zero_copy and int(stats["zero_copy_bytes"]) < 0.99 * int(stats["bytes_storage"])
             native.SAVE_PATHS.record(gpu, zero_copy, int(stats["bytes_storage"]), float(stats["seconds_total"]),
                                      warm_up)
         if root is not None:

@@ -98,9 +98,12 @@ bool box_contiguous(const tv_array_box& b, const int64_t* ext, int rank, int ite
 // Registered file mappings (tv_mapped.cpp): the registered, MAP_SHARED mapping of the
 // file open as `fd` when its inode is in the cache with exactly `size` bytes, else null.
 char* mapping_for_fd(int fd, int64_t size);
-// Map (MAP_SHARED) + register the file open as `fd` (read-write) when it lives on a
-// RAM-backed filesystem; returns the cached mapping if there is one; null when it cannot.
+// The cached registered mapping of the file open as `fd`; when there is none and the file
+// lives on a RAM-backed filesystem, queue it for background registration (the next
+// generation finds it) and return null.
 char* mapping_register_fd(int fd, int64_t size);
+int64_t registrations_pending();
+void registrations_quiesce();
 bool mappings_exist();
 void mapping_release_fd(int fd);
 void mapping_release_path(const char* path);

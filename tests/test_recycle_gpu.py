@@ -52,9 +52,14 @@ def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir, mon
     cps = helpers.checkpointables(tree, specs, rt)
     sh = helpers.shardings_for(tree, specs)
     opts = tv.SaveOptions(**c["options"])
-    # a different checkpoint of the same tree, then retired into the pool
+    # older checkpoints of the same tree, retired into the pool: the first claim of a
+    # recycled file writes it through the slot path and queues its registration, the
+    # second claim finds it registered
     tv.save_checkpoint(rt, "ckpt/old", cps, sh, opts).wait()
     delete_checkpoint(backend.store(), "ckpt/old", recycle=True)
+    tv.save_checkpoint(rt, "ckpt/older", cps, sh, opts).wait()
+    native.mapping_quiesce()
+    delete_checkpoint(backend.store(), "ckpt/older", recycle=True)
     pooled = backend.recycle_pool_bytes()
     assert pooled > 0
     before = native.totals()
@@ -111,15 +116,16 @@ def test_checkpointer_recycle_loop(shm_dir, monkeypatch):
     leaf = tv.ShardedArray("f32", s, shards)
     ck = tv.Checkpointer(rt, "run", tv.RetentionPolicy(keep_last=2), tv.SaveOptions(sync=False),
                          background_delete=True, recycle=True)
-    for step in range(6):
+    for step in range(10):  # step k reuses step k-3's files; registered from their 2nd claim
         for t in shards.values():
             t.fill_(float(step))
         ck.save_step(step, {"m": {"w": leaf}}, {"m": {"w": s}})
+        native.mapping_quiesce()
     ck.close()  # joins the save and the background retention, drains the pool
-    assert ck.all_steps() == [4, 5]
+    assert ck.all_steps() == [8, 9]
     assert backend.recycle_pool(0) is None and backend.recycle_pool(1) is None
     assert native.totals()["save"]["zero_copy_bytes"] > 0
-    for step in (4, 5):
+    for step in (8, 9):
         out = ck.load_step(step, options=tv.LoadOptions(to_host=True), current_mesh=mesh)
         assert np.all(out["m"]["w"].data == float(step))
 
@@ -140,13 +146,14 @@ def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
     rt = tv.SimulatedRuntime(c["process_count"], backend)
     cps = helpers.checkpointables(tree, specs, rt)
     sh = helpers.shardings_for(tree, specs)
-    for i in range(3):  # fresh, then over recycled (registered on first claim), then again
+    for i in range(4):  # fresh, recycled (queued for registration), then registered
         before = native.totals()["save"]
         tv.save_checkpoint(rt, "ckpt/run", cps, sh, tv.SaveOptions(**c["options"])).wait()
         after = native.totals()["save"]
+        native.mapping_quiesce()
         got = {k: v for k, v in helpers.dump_digests(backend).items() if not k.startswith(".tvpool")}
         assert got == {k: (r["size"], r["sha256"]) for k, r in gold["files"].items()}
-        if i > 0:
+        if i >= 2:
             zc = after["zero_copy_bytes"] - before["zero_copy_bytes"]
             assert (zc > 0) == (path == "zero_copy")
         delete_checkpoint(backend.store(), "ckpt/run", recycle=True)
