@@ -813,9 +813,15 @@ class SaveRun {
       box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn);
       const char* src = reinterpret_cast<const char*>(it.src.base) + boff;
       cudaEvent_t ev;
-      if (cudaMemcpyAsync(outs_[it.file].mapped + it.file_off, src, bn, cudaMemcpyDefault,
-                          ctx->zero_copy) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+      bool ok = true;
+      for (int64_t a = 0; a < bn && ok;) {  // never across a registration piece
+        const int64_t at = it.file_off + a;
+        const int64_t n = std::min(bn - a, (at / kRegisterPiece + 1) * kRegisterPiece - at);
+        ok = cudaMemcpyAsync(outs_[it.file].mapped + at, src + a, n, cudaMemcpyDefault, ctx->zero_copy) ==
+             cudaSuccess;
+        a += n;
+      }
+      if (!ok || cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventRecord(ev, ctx->zero_copy) != cudaSuccess) {
         err_.set(TV_ERR_CUDA, std::string("zero-copy D2H: ") + cudaGetErrorString(cudaGetLastError()));
         break;
@@ -1412,9 +1418,14 @@ class LoadRun {
     if (!ctx) return false;
     cudaSetDevice(it.device);
     cudaStream_t stream = ctx->stream_for(i);
-    if (cudaMemcpyAsync(st.base, src + it.in_off, it.nbytes, cudaMemcpyDefault, stream) != cudaSuccess) {
-      err_.set(TV_ERR_CUDA, std::string("zero-copy H2D: ") + cudaGetErrorString(cudaGetLastError()));
-      return false;
+    for (int64_t a = 0; a < it.nbytes;) {  // never across a registration piece
+      const int64_t at = it.in_off + a;
+      const int64_t n = std::min(it.nbytes - a, (at / kRegisterPiece + 1) * kRegisterPiece - at);
+      if (cudaMemcpyAsync(st.base + a, src + at, n, cudaMemcpyDefault, stream) != cudaSuccess) {
+        err_.set(TV_ERR_CUDA, std::string("zero-copy H2D: ") + cudaGetErrorString(cudaGetLastError()));
+        return false;
+      }
+      a += n;
     }
     dma_ += 1;
     bytes_device_ += it.nbytes;

@@ -95,6 +95,10 @@ cudaError_t launch_cast_jobs(const CastJob* dev_jobs, const CastJob* host_jobs, 
 bool box_contiguous(const tv_array_box& b, const int64_t* ext, int rank, int itemsize,
                     int64_t* byte_off, int64_t* nbytes);
 
+// Registered file mappings are registered in pieces of this many bytes (at file offsets
+// that are multiples of it); a DMA into / out of a mapping never crosses a piece boundary.
+constexpr int64_t kRegisterPiece = (int64_t)64 << 20;
+
 // Registered file mappings (tv_mapped.cpp): the registered, MAP_SHARED mapping of the
 // file open as `fd` when its inode is in the cache with exactly `size` bytes, else null.
 char* mapping_for_fd(int fd, int64_t size);

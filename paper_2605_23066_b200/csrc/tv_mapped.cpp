@@ -27,7 +27,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <deque>
 #include <cstring>
 #include <map>
@@ -103,12 +105,34 @@ class MappingCache {
 
  private:
   static void drop(const Mapping& m) {
-    cudaHostUnregister(m.addr);
+    for (int64_t off = 0; off < m.size; off += kRegisterPiece) cudaHostUnregister(m.addr + off);
     ::munmap(m.addr, (size_t)m.size);
   }
   std::mutex m_;
   std::map<std::pair<dev_t, ino_t>, Mapping> by_inode_;
 };
+
+// Register [addr, addr+size) in kRegisterPiece pieces (DMAs are split at the same file
+// offsets), pausing after each so that the registrar holds the driver at most `duty` of
+// the time: a save or restore running meanwhile keeps its CUDA calls flowing.  On failure
+// the pieces already registered are released.
+cudaError_t register_pieces(char* addr, int64_t size, double duty) {
+  for (int64_t off = 0; off < size; off += kRegisterPiece) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t ce = cudaHostRegister(addr + off, (size_t)std::min(kRegisterPiece, size - off),
+                                      cudaHostRegisterPortable);
+    if (ce != cudaSuccess) {
+      cudaGetLastError();
+      for (int64_t o = 0; o < off; o += kRegisterPiece) cudaHostUnregister(addr + o);
+      return ce;
+    }
+    if (duty < 1.0) {
+      const auto dt = std::chrono::steady_clock::now() - t0;
+      std::this_thread::sleep_for(std::chrono::duration_cast<std::chrono::microseconds>(dt * (1.0 / duty - 1.0)));
+    }
+  }
+  return cudaSuccess;
+}
 
 bool ram_backed(int fd) {
   struct statfs sf;
@@ -137,9 +161,8 @@ int register_file(const std::string& path, std::string& err) {
     ::close(fd);
     return -1;
   }
-  cudaError_t ce = cudaHostRegister(addr, (size_t)st.st_size, cudaHostRegisterPortable);
+  cudaError_t ce = register_pieces(static_cast<char*>(addr), st.st_size, 1.0);
   if (ce != cudaSuccess) {
-    cudaGetLastError();
     ::munmap(addr, (size_t)st.st_size);
     ::close(fd);
     err = "cudaHostRegister " + path + ": " + cudaGetErrorString(ce);
@@ -241,8 +264,12 @@ char* register_open(int fd, int64_t size) {
   if (char* hit = MappingCache::get().find(st.st_dev, st.st_ino, size)) return hit;
   void* addr = ::mmap(nullptr, (size_t)size, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   if (addr == MAP_FAILED) return nullptr;
-  if (cudaHostRegister(addr, (size_t)size, cudaHostRegisterPortable) != cudaSuccess) {
-    cudaGetLastError();
+  static const double duty = [] {
+    const char* v = std::getenv("TVGPU_REGISTER_DUTY");
+    const double d = v ? std::atof(v) : 0.5;
+    return d > 0 && d <= 1 ? d : 0.5;
+  }();
+  if (register_pieces(static_cast<char*>(addr), size, duty) != cudaSuccess) {
     ::munmap(addr, (size_t)size);
     return nullptr;
   }
