@@ -183,9 +183,10 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
  * (training_manager.py:262-295: a step is retired while the next is saved).
  * pool_flags & TV_POOL_REGISTER: a claimed file on a RAM-backed filesystem whose pages are
  * registered with CUDA (cached by inode) gets its contiguous items DMA'd straight into its
- * page-cache pages (zero-copy); a claimed file not registered yet is written through the
- * slot path and queued for background registration (once per file lifetime).  Without
- * the flag every output takes the pinned slot + pwrite path. */
+ * page-cache pages (zero-copy); claimed files not registered yet are registered inline up
+ * to a budget of TVGPU_REGISTER_BUDGET (default 0.25) of the save's bytes (once per file
+ * lifetime), the rest written through the slot path.  Without the flag every output takes
+ * the pinned slot + pwrite path. */
 #define TV_POOL_REGISTER 1
 int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
                           const tv_output* outputs, int n_outputs, const char* pool_dir,
@@ -228,8 +229,8 @@ int tv_pool_drain(const char* pool_dir, int64_t* freed_bytes);
 int tv_mapping_stats(int64_t* files, int64_t* bytes);
 /* Release every registered mapping (the files stay). */
 int tv_mapping_release_all(void);
-/* Wait for the background registrar (files claimed for the first time are registered off
- * the save's critical path); pending_before = files it still had queued. */
+/* Wait for any registration in flight (a background registrar; none is started by the
+ * engine today); pending_before = files still queued. */
 int tv_mapping_quiesce(int64_t* pending_before);
 
 /* ---- roofline probes (same run as the numbers they bound) ------------------------- */

@@ -713,6 +713,13 @@ class SaveRun {
   // registered, every contiguous item of the output is DMA'd straight into them and
   // never touches a pinned slot or a writer thread.
   void claim_outputs() {
+    {
+      int64_t total = 0;
+      for (int o = 0; o < n_outs_; ++o) total += outs_[o].size;
+      const char* v = std::getenv("TVGPU_REGISTER_BUDGET");
+      const double frac = v ? std::atof(v) : 0.25;
+      register_budget_.store((int64_t)(frac * (double)total));
+    }
     // outputs are claimed by a few threads (rename + open + inode lookup, and the one-time
     // registration of a file this process has not claimed before)
     std::atomic<int> next{0};
@@ -737,7 +744,19 @@ class SaveRun {
       // TV_POOL_REGISTER: zero-copy; a recycled file keeps its registration from earlier
       // generations, and the first time this process claims it, it is registered (once
       // per file lifetime).  Without the flag the output takes the slot + pwrite path.
-      if (pool_flags_ & TV_POOL_REGISTER) out.mapped = mapping_register_fd(out.fd, out.size);
+      if (pool_flags_ & TV_POOL_REGISTER) {
+        // registering a file this process has not claimed before costs about what the
+        // slot path does (pinning + mapping its pages, once per file lifetime); it is done
+        // inline — a background registrar measurably slowed concurrent saves — within a
+        // budget of TVGPU_REGISTER_BUDGET (default 1/4) of this save's bytes, so a first
+        // generation of recycled files gets registered over a few saves without one long one
+        bool now = false;
+        if (!mapping_for_fd(out.fd, out.size)) {
+          const int64_t left = register_budget_.fetch_sub(out.size);
+          now = left >= out.size;
+        }
+        out.mapped = mapping_register_fd(out.fd, out.size, now);
+      }
     }
   }
 
@@ -1177,7 +1196,7 @@ class SaveRun {
   tv_stats* stats_;
   FilePool pool_;
   const int pool_flags_;
-  std::atomic<int64_t> recycled_{0}, zero_copy_bytes_{0};
+  std::atomic<int64_t> recycled_{0}, zero_copy_bytes_{0}, register_budget_{0};
   std::vector<char> claimed_;                      // output claimed a recycled file
   std::vector<char> direct_;                       // item eligible for the zero-copy path
   std::vector<int> zq_;                            // zero-copy queue (item order)

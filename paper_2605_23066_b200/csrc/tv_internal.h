@@ -102,10 +102,9 @@ constexpr int64_t kRegisterPiece = (int64_t)64 << 20;
 // Registered file mappings (tv_mapped.cpp): the registered, MAP_SHARED mapping of the
 // file open as `fd` when its inode is in the cache with exactly `size` bytes, else null.
 char* mapping_for_fd(int fd, int64_t size);
-// The cached registered mapping of the file open as `fd`; when there is none and the file
-// lives on a RAM-backed filesystem, queue it for background registration (the next
-// generation finds it) and return null.
-char* mapping_register_fd(int fd, int64_t size);
+// The cached registered mapping of the file open (read-write) as `fd`; when there is none,
+// `register_now` and the file lives on a RAM-backed filesystem, map + register it now.
+char* mapping_register_fd(int fd, int64_t size, bool register_now);
 int64_t registrations_pending();
 void registrations_quiesce();
 bool mappings_exist();

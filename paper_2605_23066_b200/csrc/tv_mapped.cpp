@@ -264,12 +264,7 @@ char* register_open(int fd, int64_t size) {
   if (char* hit = MappingCache::get().find(st.st_dev, st.st_ino, size)) return hit;
   void* addr = ::mmap(nullptr, (size_t)size, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   if (addr == MAP_FAILED) return nullptr;
-  static const double duty = [] {
-    const char* v = std::getenv("TVGPU_REGISTER_DUTY");
-    const double d = v ? std::atof(v) : 0.5;
-    return d > 0 && d <= 1 ? d : 0.5;
-  }();
-  if (register_pieces(static_cast<char*>(addr), size, duty) != cudaSuccess) {
+  if (register_pieces(static_cast<char*>(addr), size, 1.0) != cudaSuccess) {
     ::munmap(addr, (size_t)size);
     return nullptr;
   }
@@ -282,15 +277,10 @@ char* register_open(int fd, int64_t size) {
 
 }  // namespace
 
-char* mapping_register_fd(int fd, int64_t size) {
+char* mapping_register_fd(int fd, int64_t size, bool register_now) {
   if (fd < 0) return nullptr;
   if (char* hit = mapping_for_fd(fd, size)) return hit;
-  // not registered yet: register it in the background for the next generation
-  struct stat st;
-  if (::fstat(fd, &st) != 0 || st.st_size != size || size <= 0 || !ram_backed(fd)) return nullptr;
-  const int dup = ::fcntl(fd, F_DUPFD_CLOEXEC, 0);
-  if (dup >= 0) Registrar::get().submit(dup, size);
-  return nullptr;
+  return register_now ? register_open(fd, size) : nullptr;
 }
 
 int64_t registrations_pending() { return Registrar::get().pending(); }

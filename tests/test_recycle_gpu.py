@@ -47,6 +47,7 @@ def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir, mon
     gold = json.loads((GOLDEN / f"{name}.json").read_text())
     tree, specs = cases.build_inputs(c)
     monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")  # (register=False: no zero-copy at all)
+    monkeypatch.setenv("TVGPU_REGISTER_BUDGET", "1.0")  # register every first-claimed file
     backend = tv.FilesystemBackend(shm_dir, register_pool=register)
     rt = tv.SimulatedRuntime(c["process_count"], backend)
     cps = helpers.checkpointables(tree, specs, rt)
@@ -108,6 +109,7 @@ def test_checkpointer_recycle_loop(shm_dir, monkeypatch):
     from paper_2605_23066_b200 import native
 
     monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")
+    monkeypatch.setenv("TVGPU_REGISTER_BUDGET", "1.0")
     backend = tv.FilesystemBackend(shm_dir)
     rt = tv.SimulatedRuntime(2, backend, gpus=[0])
     mesh = tv.Mesh.create([("fsdp", 2)], process_count=2)
@@ -139,6 +141,7 @@ def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
     from paper_2605_23066_b200.training_manager import delete_checkpoint
 
     monkeypatch.setenv("TVGPU_SAVE_PATH", path)
+    monkeypatch.setenv("TVGPU_REGISTER_BUDGET", "1.0")
     c = cases.case("fsdp4_per_leaf")
     gold = json.loads((GOLDEN / "fsdp4_per_leaf.json").read_text())
     tree, specs = cases.build_inputs(c)
