@@ -184,7 +184,7 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
  * pool_flags & TV_POOL_REGISTER: a claimed file on a RAM-backed filesystem whose pages are
  * registered with CUDA (cached by inode) gets its contiguous items DMA'd straight into its
  * page-cache pages (zero-copy); claimed files not registered yet are registered inline up
- * to a budget of TVGPU_REGISTER_BUDGET (default 0.25) of the save's bytes (once per file
+ * to a budget of TVGPU_REGISTER_BUDGET (default 1.0) of the save's bytes (once per file
  * lifetime), the rest written through the slot path.  Without the flag every output takes
  * the pinned slot + pwrite path. */
 #define TV_POOL_REGISTER 1

@@ -717,7 +717,7 @@ class SaveRun {
       int64_t total = 0;
       for (int o = 0; o < n_outs_; ++o) total += outs_[o].size;
       const char* v = std::getenv("TVGPU_REGISTER_BUDGET");
-      const double frac = v ? std::atof(v) : 0.25;
+      const double frac = v ? std::atof(v) : 1.0;
       register_budget_.store((int64_t)(frac * (double)total));
     }
     // outputs are claimed by a few threads (rename + open + inode lookup, and the one-time
@@ -732,6 +732,18 @@ class SaveRun {
     for (int k = 1; k < t; ++k) pool.emplace_back(work);
     work();
     for (auto& th : pool) th.join();
+    if (pool_flags_ & TV_POOL_REGISTER) {
+      // Files this process claims for the first time are registered now, one after the
+      // other (concurrent cudaHostRegister calls serialise in the driver and slow each
+      // other down; a background registrar slowed the concurrent saves): once per file
+      // lifetime, within TVGPU_REGISTER_BUDGET (default 1.0) of this save's bytes.
+      for (int o = 0; o < n_outs_ && !err_.failed.load(); ++o) {
+        OutputState& out = outs_[o];
+        if (out.fd < 0 || !claimed_[o] || out.mapped) continue;
+        if (register_budget_.fetch_sub(out.size) < out.size) continue;
+        out.mapped = mapping_register_fd(out.fd, out.size, true);
+      }
+    }
     build_zero_copy_queue();
   }
 
@@ -744,19 +756,7 @@ class SaveRun {
       // TV_POOL_REGISTER: zero-copy; a recycled file keeps its registration from earlier
       // generations, and the first time this process claims it, it is registered (once
       // per file lifetime).  Without the flag the output takes the slot + pwrite path.
-      if (pool_flags_ & TV_POOL_REGISTER) {
-        // registering a file this process has not claimed before costs about what the
-        // slot path does (pinning + mapping its pages, once per file lifetime); it is done
-        // inline — a background registrar measurably slowed concurrent saves — within a
-        // budget of TVGPU_REGISTER_BUDGET (default 1/4) of this save's bytes, so a first
-        // generation of recycled files gets registered over a few saves without one long one
-        bool now = false;
-        if (!mapping_for_fd(out.fd, out.size)) {
-          const int64_t left = register_budget_.fetch_sub(out.size);
-          now = left >= out.size;
-        }
-        out.mapped = mapping_register_fd(out.fd, out.size, now);
-      }
+      if (pool_flags_ & TV_POOL_REGISTER) out.mapped = mapping_for_fd(out.fd, out.size);
     }
   }
 
