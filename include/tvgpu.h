@@ -136,6 +136,7 @@ typedef struct tv_stats {
   double seconds_wait_slot;     /* producer: time waiting for a free pinned slot      */
   int64_t recycled_files;       /* save: outputs written over a recycled file (pool)  */
   int64_t zero_copy_bytes;      /* bytes DMA'd straight into / out of registered file pages */
+  int64_t registered_files;     /* save: recycled files registered with CUDA by this call */
 } tv_stats;
 
 typedef struct tv_engine tv_engine;
@@ -181,13 +182,14 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
  * `.partial`) and overwrites it in place — no page allocation or zeroing for storage
  * that keeps its pages (tmpfs).  Steady-state checkpointing with retention
  * (training_manager.py:262-295: a step is retired while the next is saved).
- * pool_flags & TV_POOL_REGISTER: a claimed file on a RAM-backed filesystem whose pages are
- * registered with CUDA (cached by inode) gets its contiguous items DMA'd straight into its
- * page-cache pages (zero-copy); claimed files not registered yet are registered inline up
- * to a budget of TVGPU_REGISTER_BUDGET (default 1.0) of the save's bytes (once per file
- * lifetime), the rest written through the slot path.  Without the flag every output takes
- * the pinned slot + pwrite path. */
+ * pool_flags & TV_POOL_REGISTER: claimed files on a RAM-backed filesystem not registered
+ * with CUDA yet are registered (map + cudaHostRegister, once per file lifetime, cached by
+ * inode) up to TVGPU_REGISTER_BUDGET (default 0.5) of the save's bytes.
+ * pool_flags & TV_POOL_ZERO_COPY: the contiguous items of a claimed, registered file are
+ * DMA'd straight into its page-cache pages (zero-copy); everything else takes the pinned
+ * slot + pwrite path. */
 #define TV_POOL_REGISTER 1
+#define TV_POOL_ZERO_COPY 2
 int tv_engine_save_pooled(tv_engine* e, const tv_write_item* items, int n_items,
                           const tv_output* outputs, int n_outputs, const char* pool_dir,
                           int pool_flags, tv_stats* stats);

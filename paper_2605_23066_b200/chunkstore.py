@@ -625,13 +625,15 @@ def execute_writes(store: Store, pending: list[_PendingChunk], engine_cfg=None, 
         pool = backend.recycle_pool(process_of_key(out_keys[0])) if root is not None else None
         # per GPU and save size (rates of a 4 GB and an 80 GB save are not comparable)
         gpu = (int(pending[0].region.gpu), max(1, sum(sizes)).bit_length())
-        zero_copy = bool(pool) and bool(getattr(backend, "register_pool", False)) and native.SAVE_PATHS.choose(gpu)
+        register = bool(pool) and bool(getattr(backend, "register_pool", False))
+        zero_copy = register and native.SAVE_PATHS.choose(gpu)
         with native.engine_lease(cfg, concurrent) as eng:
-            stats = eng.save(items, outputs, pool, register=zero_copy)
+            stats = eng.save(items, outputs, pool, register=register, zero_copy=zero_copy)
         if pool and int(stats["recycled_files"]) > 0:
-            # a zero-copy save that found unregistered files wrote those through the slot
-            # path (they are being registered in the background): a warm-up, not scored
-            warm_up = zero_copy and int(stats["zero_copy_bytes"]) < 0.99 * int(stats["bytes_storage"])
+            # a save that registered files (once per file lifetime) or, zero-copy, still
+            # found unregistered ones is a warm-up: not scored
+            warm_up = int(stats["registered_files"]) > 0 or (
+                zero_copy and int(stats["zero_copy_bytes"]) < 0.99 * int(stats["bytes_storage"]))
             native.SAVE_PATHS.record(gpu, zero_copy, int(stats["bytes_storage"]), float(stats["seconds_total"]),
                                      warm_up)
         if root is not None:

@@ -717,7 +717,7 @@ class SaveRun {
       int64_t total = 0;
       for (int o = 0; o < n_outs_; ++o) total += outs_[o].size;
       const char* v = std::getenv("TVGPU_REGISTER_BUDGET");
-      const double frac = v ? std::atof(v) : 1.0;
+      const double frac = v ? std::atof(v) : 0.5;
       register_budget_.store((int64_t)(frac * (double)total));
     }
     // outputs are claimed by a few threads (rename + open + inode lookup, and the one-time
@@ -736,14 +736,19 @@ class SaveRun {
       // Files this process claims for the first time are registered now, one after the
       // other (concurrent cudaHostRegister calls serialise in the driver and slow each
       // other down; a background registrar slowed the concurrent saves): once per file
-      // lifetime, within TVGPU_REGISTER_BUDGET (default 1.0) of this save's bytes.
+      // lifetime, within TVGPU_REGISTER_BUDGET (default 0.5) of this save's bytes, so a
+      // generation of recycled files is registered over a couple of saves.
       for (int o = 0; o < n_outs_ && !err_.failed.load(); ++o) {
         OutputState& out = outs_[o];
         if (out.fd < 0 || !claimed_[o] || out.mapped) continue;
         if (register_budget_.fetch_sub(out.size) < out.size) continue;
         out.mapped = mapping_register_fd(out.fd, out.size, true);
+        registered_now_ += 1;
       }
     }
+    // registered outputs take the zero-copy path only when this save chose it
+    if (!(pool_flags_ & TV_POOL_ZERO_COPY))
+      for (int o = 0; o < n_outs_; ++o) outs_[o].mapped = nullptr;
     build_zero_copy_queue();
   }
 
@@ -756,7 +761,7 @@ class SaveRun {
       // TV_POOL_REGISTER: zero-copy; a recycled file keeps its registration from earlier
       // generations, and the first time this process claims it, it is registered (once
       // per file lifetime).  Without the flag the output takes the slot + pwrite path.
-      if (pool_flags_ & TV_POOL_REGISTER) out.mapped = mapping_for_fd(out.fd, out.size);
+      if (pool_flags_ & (TV_POOL_REGISTER | TV_POOL_ZERO_COPY)) out.mapped = mapping_for_fd(out.fd, out.size);
     }
   }
 
@@ -1196,7 +1201,7 @@ class SaveRun {
   tv_stats* stats_;
   FilePool pool_;
   const int pool_flags_;
-  std::atomic<int64_t> recycled_{0}, zero_copy_bytes_{0}, register_budget_{0};
+  std::atomic<int64_t> recycled_{0}, zero_copy_bytes_{0}, register_budget_{0}, registered_now_{0};
   std::vector<char> claimed_;                      // output claimed a recycled file
   std::vector<char> direct_;                       // item eligible for the zero-copy path
   std::vector<int> zq_;                            // zero-copy queue (item order)

@@ -28,6 +28,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libtvgpu.so"
 TV_OK = 0
 TV_ERR_IO = -2  # include/tvgpu.h
 POOL_REGISTER = 1  # TV_POOL_REGISTER
+POOL_ZERO_COPY = 2  # TV_POOL_ZERO_COPY
 
 # ---- C struct layouts -------------------------------------------------------------------
 
@@ -60,7 +61,7 @@ STATS = np.dtype(
      ("kernel_launches", "<i8"), ("dma_copies", "<i8"), ("files", "<i8"),
      ("seconds_total", "<f8"), ("seconds_kernel", "<f8"), ("seconds_io", "<f8"),
      ("seconds_wait_dma", "<f8"), ("seconds_wait_slot", "<f8"), ("recycled_files", "<i8"),
-     ("zero_copy_bytes", "<i8")],
+     ("zero_copy_bytes", "<i8"), ("registered_files", "<i8")],
     align=True,
 )
 
@@ -235,7 +236,7 @@ def write_table(src_base, src_shape, src_off, ext, itemsize, file, device, file_
 # transfers its timed region issued).
 _FIELDS = ("kernel_launches", "dma_copies", "bytes_device", "bytes_storage", "bytes_packed", "files",
            "seconds_total", "seconds_io", "seconds_wait_dma", "seconds_wait_slot", "recycled_files",
-           "zero_copy_bytes")
+           "zero_copy_bytes", "registered_files")
 TOTALS = {"save": dict.fromkeys(_FIELDS, 0), "load": dict.fromkeys(_FIELDS, 0),
           "kernels": {"kernel_launches": 0}, "peer": {"bytes": 0}}
 _totals_lock = threading.Lock()
@@ -507,14 +508,14 @@ class Engine:
             self._h = None
 
     def save(self, items: np.ndarray, outputs: np.ndarray, pool_dir: str | None = None,
-             register: bool = False) -> np.ndarray:
+             register: bool = False, zero_copy: bool = False) -> np.ndarray:
         """Write every item into its output; with ``pool_dir`` outputs reuse recycled
-        files of their exact size, and with ``register`` DMA straight into their
-        registered page-cache pages (see tv_engine_save_pooled)."""
+        files of their exact size; ``register`` registers first-claimed ones with CUDA,
+        ``zero_copy`` DMAs straight into registered ones (see tv_engine_save_pooled)."""
         stats = np.zeros(1, STATS)
         items = np.ascontiguousarray(items, WRITE_ITEM)
         outputs = np.ascontiguousarray(outputs, OUTPUT)
-        flags = POOL_REGISTER if register else 0
+        flags = (POOL_REGISTER if register else 0) | (POOL_ZERO_COPY if zero_copy else 0)
         with _bound_to(self.cpus):
             rc = lib().tv_engine_save_pooled(self._h, _ptr(items), len(items), _ptr(outputs), len(outputs),
                                              pool_dir.encode() if pool_dir else None, flags,

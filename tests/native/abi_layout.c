@@ -23,6 +23,6 @@ int main(void) {
   printf("tv_stats %zu\n", sizeof(tv_stats));
   F(tv_stats, bytes_device); F(tv_stats, seconds_total); F(tv_stats, seconds_kernel);
   F(tv_stats, seconds_io); F(tv_stats, seconds_wait_dma); F(tv_stats, seconds_wait_slot);
-  F(tv_stats, recycled_files); F(tv_stats, zero_copy_bytes);
+  F(tv_stats, recycled_files); F(tv_stats, zero_copy_bytes); F(tv_stats, registered_files);
   return 0;
 }
