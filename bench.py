@@ -714,6 +714,12 @@ def run_ours(args) -> dict:
     reshard = (reshard_leg(tv, native, d, rt, wl, state, shardings, args, N, base)
                if args.reshard_steps > 0 and wl.name == "c2" else None)
     free_recycle_pool(native, d, backend)  # the main tree's retired files: not needed again
+    # The short legs below recycle files but do not register them with CUDA: registering a
+    # file pays off over many saves of it (the main loop's steady state), not over the
+    # e2e leg's few steps, and in a training loop it would lengthen the first background
+    # saves past the step (C5 measures exactly that blocking).  FilesystemBackend(
+    # register_pool=False) is the same choice for a user.
+    backend.register_pool = False
     e2e = end_to_end(tv, rt, wl, args, d, base) if not args.no_e2e else None
     free_recycle_pool(native, d, backend)
     c5 = None
@@ -755,6 +761,7 @@ def run_ours(args) -> dict:
         "restore_ms": round(restore_ms, 2),
         "retire_ms": round(retire_ms, 2),
         "recycle": {"enabled": bool(args.recycle),
+                    "register_pool": "main C2 loop only (not the e2e / C5 / C1 legs)",
                     "save_path_rates_rank0": native.SAVE_PATHS.snapshot(),
                     "files_overwritten_in_timed_steps": int(d.sum(after["save"]["recycled_files"]
                                                                   - before["save"]["recycled_files"])),

@@ -184,7 +184,7 @@ int tv_engine_save(tv_engine* e, const tv_write_item* items, int n_items,
  * (training_manager.py:262-295: a step is retired while the next is saved).
  * pool_flags & TV_POOL_REGISTER: claimed files on a RAM-backed filesystem not registered
  * with CUDA yet are registered (map + cudaHostRegister, once per file lifetime, cached by
- * inode) up to TVGPU_REGISTER_BUDGET (default 0.5) of the save's bytes.
+ * inode) up to TVGPU_REGISTER_BUDGET (default 1.0) of the save's bytes.
  * pool_flags & TV_POOL_ZERO_COPY: the contiguous items of a claimed, registered file are
  * DMA'd straight into its page-cache pages (zero-copy); everything else takes the pinned
  * slot + pwrite path. */

@@ -717,7 +717,7 @@ class SaveRun {
       int64_t total = 0;
       for (int o = 0; o < n_outs_; ++o) total += outs_[o].size;
       const char* v = std::getenv("TVGPU_REGISTER_BUDGET");
-      const double frac = v ? std::atof(v) : 0.5;
+      const double frac = v ? std::atof(v) : 1.0;
       register_budget_.store((int64_t)(frac * (double)total));
     }
     // outputs are claimed by a few threads (rename + open + inode lookup, and the one-time
@@ -736,8 +736,7 @@ class SaveRun {
       // Files this process claims for the first time are registered now, one after the
       // other (concurrent cudaHostRegister calls serialise in the driver and slow each
       // other down; a background registrar slowed the concurrent saves): once per file
-      // lifetime, within TVGPU_REGISTER_BUDGET (default 0.5) of this save's bytes, so a
-      // generation of recycled files is registered over a couple of saves.
+      // lifetime, within TVGPU_REGISTER_BUDGET (default 1.0) of this save's bytes.
       for (int o = 0; o < n_outs_ && !err_.failed.load(); ++o) {
         OutputState& out = outs_[o];
         if (out.fd < 0 || !claimed_[o] || out.mapped) continue;
