@@ -761,7 +761,7 @@ def run_ours(args) -> dict:
         "restore_ms": round(restore_ms, 2),
         "retire_ms": round(retire_ms, 2),
         "recycle": {"enabled": bool(args.recycle),
-                    "register_pool": "main C2 loop only (not the e2e / C5 / C1 legs)",
+                    "register_pool": "main C2 loop and C1 leg (not the e2e / C5 legs)",
                     "save_path_rates_rank0": native.SAVE_PATHS.snapshot(),
                     "files_overwritten_in_timed_steps": int(d.sum(after["save"]["recycled_files"]
                                                                   - before["save"]["recycled_files"])),
