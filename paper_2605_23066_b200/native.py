@@ -415,11 +415,21 @@ class SavePathChooser:
             return rz is None
 
     def record(self, key, zero_copy: bool, nbytes: int, seconds: float, warm_up: bool) -> None:
-        if warm_up or seconds <= 0 or nbytes <= 0:
+        """Score a save.  Warm-ups (files registered) are not scored, and neither is the
+        first zero-copy save after one: the first DMA into freshly registered pages runs
+        at a fraction of the link rate (the I/O mappings are populated on first touch)."""
+        if seconds <= 0 or nbytes <= 0:
             return
         gpu = key[0] if isinstance(key, tuple) else key
         rate = nbytes / seconds
         with self._lock:
+            st = self._entry(key)
+            if warm_up:
+                st["skip_zc"] = 1
+                return
+            if zero_copy and st.get("skip_zc", 1) > 0:
+                st["skip_zc"] = st.get("skip_zc", 1) - 1
+                return
             for k in (key, ("gpu", gpu)):
                 st = self._entry(k)
                 old = st["rate"][zero_copy]

@@ -76,6 +76,8 @@ def test_save_path_chooser_explores_then_exploits(monkeypatch):
     assert c.choose(key) is True                      # explore zero-copy first
     c.record(key, True, 10 << 30, 1.0, warm_up=True)  # registered new files: not scored
     assert c.choose(key) is True
+    c.record(key, True, 15 << 30, 1.0, warm_up=False)  # first touch of new registrations: not scored
+    assert c.choose(key) is True
     c.record(key, True, 50 << 30, 1.0, warm_up=False)
     assert c.choose(key) is False                     # then the slot path
     c.record(key, False, 30 << 30, 1.0, warm_up=False)
@@ -84,6 +86,7 @@ def test_save_path_chooser_explores_then_exploits(monkeypatch):
     assert c.choose((0, 33)) is True
     # a close call is re-tried once every RETRY saves
     close = (2, 37)
+    c.record(close, True, 50 << 30, 1.0, warm_up=False)  # (discarded: first zero-copy sample)
     c.record(close, True, 50 << 30, 1.0, warm_up=False)
     c.record(close, False, 45 << 30, 1.0, warm_up=False)
     picks = [c.choose(close) for _ in range(c.RETRY)]
