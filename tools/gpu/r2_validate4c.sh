@@ -1,0 +1,6 @@
+set -x
+timeout 1800 python -m pytest tests -m gpu -q -x > gpurun_out/r2_v4c_gputests.log 2>&1; echo tests rc=$?; tail -3 gpurun_out/r2_v4c_gputests.log
+timeout 1500 python bench.py --gpus 2 --steps 10 > gpurun_out/r2_v4c_n2.json 2> gpurun_out/r2_v4c_n2.err; echo n2 rc=$?
+timeout 1500 python bench.py --gpus 4 --steps 10 > gpurun_out/r2_v4c_n4.json 2> gpurun_out/r2_v4c_n4.err; echo n4 rc=$?
+timeout 1500 python bench.py --gpus 4 --config c3 --steps 5 --c5-layers 0 --reshard-steps 0 --no-e2e --c1-steps 0 > gpurun_out/r2_v4c_c3.json 2> gpurun_out/r2_v4c_c3.err; echo c3 rc=$?
+timeout 1500 python bench.py --gpus 4 --config c4 --steps 5 --c5-layers 0 --reshard-steps 0 --no-e2e --c1-steps 0 > gpurun_out/r2_v4c_c4.json 2> gpurun_out/r2_v4c_c4.err; echo c4 rc=$?
