@@ -532,8 +532,8 @@ def run_ours(args) -> dict:
         # save overwrites them in place (steady-state checkpointing with max_to_keep)
         d.barrier()
         tr = time.perf_counter()
+        retire_checkpoint(d, backend, path, args.recycle)
         if d.rank == 0:
-            delete_checkpoint(backend.store("retention"), path, recycle=args.recycle)
             shutil.rmtree(os.path.join(base, path), ignore_errors=True)  # emptied dirs
         retire_ms = d.max((time.perf_counter() - tr) * 1e3)
         d.barrier()
@@ -1185,6 +1185,28 @@ def kernel_roofline(tv, native, state, rt, d, ksave: dict, kload: dict, args, st
         "host_enqueue_ms": round(host_ms, 3),
         "launches_in_timed_region": 0,
     }
+
+
+def retire_checkpoint(d, backend, path: str, recycle: bool) -> None:
+    """Retire a checkpoint as retention would (``training_manager.delete_checkpoint``:
+    finality marker first, then everything else), the bulk spread over the ranks: under
+    torchrun process 0 removes the marker, then every rank its own ``process_<p>/`` files
+    in parallel, then process 0 the remaining top-level documents."""
+    from paper_2605_23066_b200.training_manager import _finality_marker, delete_checkpoint
+
+    store = backend.store("retention")
+    if not d.on:
+        delete_checkpoint(store, path, recycle=recycle)
+        return
+    if d.rank == 0:
+        marker = f"{path}/{_finality_marker(store)}"
+        if store.exists(marker):
+            store.delete(marker)
+    d.barrier()
+    delete_checkpoint(store, f"{path}/process_{d.rank}", recycle=recycle)
+    d.barrier()
+    if d.rank == 0:
+        delete_checkpoint(store, path, recycle=recycle)
 
 
 def c1_leg(tv, native, d, base: str, args) -> dict | None:
