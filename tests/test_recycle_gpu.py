@@ -160,3 +160,43 @@ def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
             zc = after["zero_copy_bytes"] - before["zero_copy_bytes"]
             assert (zc > 0) == (path == "zero_copy")
         delete_checkpoint(backend.store(), "ckpt/run", recycle=True)
+
+
+def test_registrations_released_by_unlink_and_cold_restore(shm_dir, monkeypatch):
+    """A checkpoint written zero-copy restores correctly after the process dropped every
+    registration (a fresh process: pread path), and deleting it without recycling
+    releases the registrations of its files."""
+    import numpy as np
+    import torch
+
+    import paper_2605_23066_b200 as tv
+    from paper_2605_23066_b200 import native
+    from paper_2605_23066_b200.training_manager import delete_checkpoint
+
+    monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")
+    monkeypatch.setenv("TVGPU_REGISTER_BUDGET", "1.0")
+    native.lib().tv_mapping_release_all()
+    backend = tv.FilesystemBackend(shm_dir)
+    rt = tv.SimulatedRuntime(1, backend, gpus=[0])
+    mesh = tv.Mesh.create([("fsdp", 1)], process_count=1)
+    s = tv.Sharding(mesh, tv.PartitionSpec(("fsdp", None)), (1024, 1024))
+    w = torch.randn(1024, 1024, device="cuda")
+    leaf = tv.ShardedArray("f32", s, {0: w})
+    for name in ("a", "b"):  # a: fresh; b: claims a's files and registers them
+        tv.save_checkpoint(rt, name, {"m": {"w": leaf}}, {"m": {"w": s}}).wait()
+        delete_checkpoint(backend.store(), name, recycle=True)
+    before = native.totals()["save"]["zero_copy_bytes"]
+    tv.save_checkpoint(rt, "c", {"m": {"w": leaf}}, {"m": {"w": s}}).wait()
+    assert native.totals()["save"]["zero_copy_bytes"] > before
+    files, nbytes = native.mapping_stats()
+    assert files >= 1 and nbytes >= w.numel() * 4
+    native.lib().tv_mapping_release_all()  # "a new process": nothing registered
+    assert native.mapping_stats() == (0, 0)
+    out = tv.load_checkpoint(rt, "c", None, tv.LoadOptions(to_host=True), current_mesh=mesh)
+    assert np.array_equal(out["m"]["w"].data, w.cpu().numpy())
+    # registered again by a save over recycled files, then freed by a plain delete
+    delete_checkpoint(backend.store(), "c", recycle=True)
+    tv.save_checkpoint(rt, "d", {"m": {"w": leaf}}, {"m": {"w": s}}).wait()
+    assert native.mapping_stats()[0] >= 1
+    delete_checkpoint(backend.store(), "d", recycle=False)
+    assert native.mapping_stats() == (0, 0)
