@@ -110,7 +110,7 @@ def test_checkpointer_recycle_loop(shm_dir, monkeypatch):
 
     monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")
     monkeypatch.setenv("TVGPU_REGISTER_BUDGET", "1.0")
-    backend = tv.FilesystemBackend(shm_dir)
+    backend = tv.FilesystemBackend(shm_dir, register_pool=True)
     rt = tv.SimulatedRuntime(2, backend, gpus=[0])
     mesh = tv.Mesh.create([("fsdp", 2)], process_count=2)
     s = tv.Sharding(mesh, tv.PartitionSpec(("fsdp", None)), (256, 128))
@@ -145,7 +145,7 @@ def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
     c = cases.case("fsdp4_per_leaf")
     gold = json.loads((GOLDEN / "fsdp4_per_leaf.json").read_text())
     tree, specs = cases.build_inputs(c)
-    backend = tv.FilesystemBackend(shm_dir)
+    backend = tv.FilesystemBackend(shm_dir, register_pool=True)
     rt = tv.SimulatedRuntime(c["process_count"], backend)
     cps = helpers.checkpointables(tree, specs, rt)
     sh = helpers.shardings_for(tree, specs)
@@ -176,7 +176,7 @@ def test_registrations_released_by_unlink_and_cold_restore(shm_dir, monkeypatch)
     monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")
     monkeypatch.setenv("TVGPU_REGISTER_BUDGET", "1.0")
     native.lib().tv_mapping_release_all()
-    backend = tv.FilesystemBackend(shm_dir)
+    backend = tv.FilesystemBackend(shm_dir, register_pool=True)
     rt = tv.SimulatedRuntime(1, backend, gpus=[0])
     mesh = tv.Mesh.create([("fsdp", 1)], process_count=1)
     s = tv.Sharding(mesh, tv.PartitionSpec(("fsdp", None)), (1024, 1024))
