@@ -716,13 +716,12 @@ def run_ours(args) -> dict:
     reshard = (reshard_leg(tv, native, d, rt, wl, state, shardings, args, N, base)
                if args.reshard_steps > 0 and wl.name == "c2" else None)
     free_recycle_pool(native, d, backend)  # the main tree's retired files: not needed again
-    # The short legs below recycle files but do not register them with CUDA: registering a
-    # file pays off over many saves of it (the main loop's steady state), not over the
-    # e2e leg's few steps, and in a training loop it would lengthen the first background
-    # saves past the step (C5 measures exactly that blocking).  FilesystemBackend(
-    # register_pool=False) is the same choice for a user.
-    backend.register_pool = False
+    # the e2e leg is the same steady state through host buffers (its own warm-up registers
+    # its files); the C5 loop below recycles without registering: in a training loop the
+    # one-time registration would lengthen the first background saves past the step,
+    # which is exactly the blocking C5 measures (FilesystemBackend(register_pool=False))
     e2e = end_to_end(tv, rt, wl, args, d, base) if not args.no_e2e else None
+    backend.register_pool = False
     free_recycle_pool(native, d, backend)
     c5 = None
     if args.c5_layers > 0 and wl.name == "c2":
@@ -763,7 +762,7 @@ def run_ours(args) -> dict:
         "restore_ms": round(restore_ms, 2),
         "retire_ms": round(retire_ms, 2),
         "recycle": {"enabled": bool(args.recycle),
-                    "register_pool": "main C2 loop only (FilesystemBackend(register_pool=True)); the e2e, C5 and C1 legs recycle without registering",
+                    "register_pool": "main C2 loop and the e2e leg (FilesystemBackend(register_pool=True)); the C5 and C1 legs recycle without registering",
                     "save_path_rates_rank0": native.SAVE_PATHS.snapshot(),
                     "files_overwritten_in_timed_steps": int(d.sum(after["save"]["recycled_files"]
                                                                   - before["save"]["recycled_files"])),
@@ -1442,7 +1441,7 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
     torch.cuda.synchronize()
     tree_bytes = sum(nbytes(s, dt) for _, _, s, dt in e_leaves)
     times = []
-    for i in range(args.e2e_steps + 1):
+    for i in range(args.e2e_warmup + args.e2e_steps):
         d.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -1467,7 +1466,7 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
             delete_checkpoint(rt.backend.store("retention"), path, recycle=args.recycle)
         dt = d.max(time.perf_counter() - t0)
         d.barrier()
-        if i > 0:
+        if i >= args.e2e_warmup:
             times.append(dt)
     del state, host
     torch.cuda.empty_cache()
@@ -1485,6 +1484,7 @@ def end_to_end(tv, rt, wl, args, d, base) -> dict:
         "api": f"save_checkpoint({args.save_mode}) + wait() + load_checkpoint + retire, with H2D of the "
                "inputs and D2H of the restored shards (pinned) inside the timed region",
         "steps": args.e2e_steps,
+        "warmup": args.e2e_warmup,
     }
 
 
@@ -1689,6 +1689,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-warmup", type=int, default=3)
     ap.add_argument("--cpu-layers", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dir", default="/dev/shm/tvbench")
