@@ -762,7 +762,7 @@ def run_ours(args) -> dict:
         "restore_ms": round(restore_ms, 2),
         "retire_ms": round(retire_ms, 2),
         "recycle": {"enabled": bool(args.recycle),
-                    "register_pool": "main C2 loop and the e2e leg (FilesystemBackend(register_pool=True)); the C5 and C1 legs recycle without registering",
+                    "register_pool": "main C2 loop, e2e and C1 legs (FilesystemBackend(register_pool=True)); the C5 loop recycles without registering",
                     "save_path_rates_rank0": native.SAVE_PATHS.snapshot(),
                     "files_overwritten_in_timed_steps": int(d.sum(after["save"]["recycled_files"]
                                                                   - before["save"]["recycled_files"])),
@@ -1225,7 +1225,7 @@ def c1_leg(tv, native, d, base: str, args) -> dict | None:
         return None
     gpu = d.local if d.on else 0
     sub = os.path.join(base, "c1leg")
-    backend = tv.FilesystemBackend(sub)
+    backend = tv.FilesystemBackend(sub, register_pool=bool(args.recycle) and not args.no_register)
     rt = tv.SimulatedRuntime(1, backend, gpus=[gpu])
     gen = torch.Generator(device=f"cuda:{gpu}")
     gen.manual_seed(0)
