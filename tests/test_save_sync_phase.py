@@ -55,3 +55,18 @@ def test_caller_streams_without_gpu():
         gpus = [0]
 
     assert sp.caller_streams(RT()) == {}
+
+
+def test_reference_defaults_switch_load_options():
+    from paper_2605_23066_b200 import compat
+    from paper_2605_23066_b200.load_pipeline import LoadOptions, reference_defaults
+
+    assert LoadOptions().to_host is False and LoadOptions().read_once is True
+    reference_defaults(True)
+    try:
+        assert compat.enabled()
+        assert LoadOptions().to_host is True and LoadOptions().read_once is False
+        assert LoadOptions(read_once=True).read_once is True  # explicit values still win
+    finally:
+        reference_defaults(False)
+    assert LoadOptions().to_host is False
