@@ -231,9 +231,6 @@ int tv_pool_drain(const char* pool_dir, int64_t* freed_bytes);
 int tv_mapping_stats(int64_t* files, int64_t* bytes);
 /* Release every registered mapping (the files stay). */
 int tv_mapping_release_all(void);
-/* Wait for any registration in flight (a background registrar; none is started by the
- * engine today); pending_before = files still queued. */
-int tv_mapping_quiesce(int64_t* pending_before);
 
 /* ---- roofline probes (same run as the numbers they bound) ------------------------- */
 /* fio-style sequential write then read of n_threads files of file_bytes each, in

@@ -720,8 +720,7 @@ class SaveRun {
       const double frac = v ? std::atof(v) : 1.0;
       register_budget_.store((int64_t)(frac * (double)total));
     }
-    // outputs are claimed by a few threads (rename + open + inode lookup, and the one-time
-    // registration of a file this process has not claimed before)
+    // outputs are claimed by a few threads (rename + open + inode lookup)
     std::atomic<int> next{0};
     auto work = [&] {
       for (int o = next.fetch_add(1); o < n_outs_ && !err_.failed.load(); o = next.fetch_add(1))
@@ -752,16 +751,12 @@ class SaveRun {
   }
 
   void claim_output(int o) {
-    {
-      OutputState& out = outs_[o];
-      if (out.path.empty() || out.size == 0) return;
-      std::call_once(out.opened, [&] { open_output(out); });
-      if (out.fd < 0 || !claimed_[o]) return;
-      // TV_POOL_REGISTER: zero-copy; a recycled file keeps its registration from earlier
-      // generations, and the first time this process claims it, it is registered (once
-      // per file lifetime).  Without the flag the output takes the slot + pwrite path.
-      if (pool_flags_ & (TV_POOL_REGISTER | TV_POOL_ZERO_COPY)) out.mapped = mapping_for_fd(out.fd, out.size);
-    }
+    OutputState& out = outs_[o];
+    if (out.path.empty() || out.size == 0) return;
+    std::call_once(out.opened, [&] { open_output(out); });
+    if (out.fd < 0 || !claimed_[o]) return;
+    // a recycled file keeps its registration from earlier generations (cached by inode)
+    if (pool_flags_ & (TV_POOL_REGISTER | TV_POOL_ZERO_COPY)) out.mapped = mapping_for_fd(out.fd, out.size);
   }
 
   void build_zero_copy_queue() {

@@ -105,8 +105,6 @@ char* mapping_for_fd(int fd, int64_t size);
 // The cached registered mapping of the file open (read-write) as `fd`; when there is none,
 // `register_now` and the file lives on a RAM-backed filesystem, map + register it now.
 char* mapping_register_fd(int fd, int64_t size, bool register_now);
-int64_t registrations_pending();
-void registrations_quiesce();
 bool mappings_exist();
 void mapping_release_fd(int fd);
 void mapping_release_path(const char* path);

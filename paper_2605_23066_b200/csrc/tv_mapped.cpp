@@ -28,9 +28,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
-#include <condition_variable>
 #include <cstdlib>
-#include <deque>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -196,65 +194,6 @@ std::vector<std::string> pool_files(const std::string& pool) {
   return out;
 }
 
-char* register_open(int fd, int64_t size);
-
-// Background registrar: a recycled file claimed for the first time is registered here,
-// off the save's critical path (cudaHostRegister pins and maps every page: ~0.5-1 s for a
-// few tens of GB, and it serialises with other CUDA calls of the process); the save that
-// claimed it uses the slot path, the next generation finds it registered.
-class Registrar {
- public:
-  static Registrar& get() {
-    static Registrar* r = new Registrar();  // process lifetime
-    return *r;
-  }
-  // Take ownership of `fd` (a dup of the claimed file) and register it in the background.
-  void submit(int fd, int64_t size) {
-    {
-      std::lock_guard<std::mutex> g(m_);
-      q_.push_back({fd, size});
-      if (!started_) {
-        started_ = true;
-        std::thread([this] { loop(); }).detach();
-      }
-    }
-    cv_.notify_one();
-  }
-  int64_t pending() {
-    std::lock_guard<std::mutex> g(m_);
-    return (int64_t)q_.size() + busy_;
-  }
-  // Wait until every submitted file is registered (before drains, releases, exit).
-  void quiesce() {
-    std::unique_lock<std::mutex> g(m_);
-    idle_.wait(g, [&] { return q_.empty() && busy_ == 0; });
-  }
-
- private:
-  void loop() {
-    for (;;) {
-      std::pair<int, int64_t> job;
-      {
-        std::unique_lock<std::mutex> g(m_);
-        cv_.wait(g, [&] { return !q_.empty(); });
-        job = q_.front();
-        q_.pop_front();
-        busy_ = 1;
-      }
-      register_open(job.first, job.second);
-      ::close(job.first);
-      std::lock_guard<std::mutex> g(m_);
-      busy_ = 0;
-      if (q_.empty()) idle_.notify_all();
-    }
-  }
-  std::mutex m_;
-  std::condition_variable cv_, idle_;
-  std::deque<std::pair<int, int64_t>> q_;
-  bool started_ = false;
-  int busy_ = 0;
-};
-
 // Map + register the file open (read-write) as `fd`; the cached address or null.
 char* register_open(int fd, int64_t size) {
   struct stat st;
@@ -283,8 +222,6 @@ char* mapping_register_fd(int fd, int64_t size, bool register_now) {
   return register_now ? register_open(fd, size) : nullptr;
 }
 
-int64_t registrations_pending() { return Registrar::get().pending(); }
-void registrations_quiesce() { Registrar::get().quiesce(); }
 
 char* mapping_for_fd(int fd, int64_t size) {
   if (fd < 0 || MappingCache::get().empty()) return nullptr;
@@ -358,7 +295,6 @@ int tv_pool_drain(const char* pool_dir, int64_t* freed_bytes) {
     tv::set_error("tv_pool_drain: bad arguments");
     return TV_ERR_ARG;
   }
-  tv::registrations_quiesce();  // no registration of a file being drained is in flight
   int64_t freed = 0;
   for (const std::string& f : tv::pool_files(pool_dir)) {
     struct stat st;
@@ -377,14 +313,7 @@ int tv_mapping_stats(int64_t* files, int64_t* bytes) {
 
 int tv_mapping_release_all(void) {
   tv::DeviceGuard guard;
-  tv::registrations_quiesce();
   tv::MappingCache::get().release_all();
-  return TV_OK;
-}
-
-int tv_mapping_quiesce(int64_t* pending_before) {
-  if (pending_before) *pending_before = tv::registrations_pending();
-  tv::registrations_quiesce();
   return TV_OK;
 }
 

@@ -73,7 +73,7 @@ EXPORTS = (
     "tv_ipc_export", "tv_ipc_import", "tv_ipc_close", "tv_probe_storage", "tv_probe_pcie",
     "tv_unlink_many", "tv_probe_storage_dma", "tv_engine_save_pooled", "tv_recycle_many",
     "tv_probe_storage_rewrite", "tv_pool_register", "tv_pool_drain", "tv_mapping_stats",
-    "tv_mapping_release_all", "tv_mapping_quiesce",
+    "tv_mapping_release_all",
 )
 
 _lib = None
@@ -107,7 +107,6 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tv_pool_drain": (I, [ctypes.c_char_p, ctypes.POINTER(L)]),
         "tv_mapping_stats": (I, [ctypes.POINTER(L), ctypes.POINTER(L)]),
         "tv_mapping_release_all": (I, []),
-        "tv_mapping_quiesce": (I, [ctypes.POINTER(L)]),
         "tv_probe_storage_rewrite": (I, [ctypes.c_char_p, I, L, L, ctypes.POINTER(D), ctypes.POINTER(D),
                                          ctypes.POINTER(D)]),
         "tv_probe_storage_dma": (I, [ctypes.c_char_p, I, L, L, I, ctypes.POINTER(D), ctypes.POINTER(D),
@@ -139,10 +138,6 @@ def lib() -> ctypes.CDLL:
             if handle.tv_abi_version() != 2:
                 raise NativeError("libtvgpu ABI version mismatch")
             _lib = handle
-            import atexit
-
-            # no background registration may be in flight while CUDA tears down
-            atexit.register(lambda: handle.tv_mapping_quiesce(None))
     return _lib
 
 
@@ -353,13 +348,6 @@ def pool_drain(pool_dir: str) -> int:
     """Release the registrations of, and unlink, every pool file; bytes freed."""
     n = ctypes.c_int64()
     check(lib().tv_pool_drain(pool_dir.encode(), ctypes.byref(n)), "tv_pool_drain")
-    return n.value
-
-
-def mapping_quiesce() -> int:
-    """Wait for the background registrar; files it still had queued."""
-    n = ctypes.c_int64()
-    check(lib().tv_mapping_quiesce(ctypes.byref(n)), "tv_mapping_quiesce")
     return n.value
 
 

@@ -54,12 +54,11 @@ def test_save_over_recycled_files_is_byte_identical(name, register, shm_dir, mon
     sh = helpers.shardings_for(tree, specs)
     opts = tv.SaveOptions(**c["options"])
     # older checkpoints of the same tree, retired into the pool: the first claim of a
-    # recycled file writes it through the slot path and queues its registration, the
-    # second claim finds it registered
+    # recycled file registers it (and writes it through the slot path... or zero-copy
+    # right away), the second claim finds it registered
     tv.save_checkpoint(rt, "ckpt/old", cps, sh, opts).wait()
     delete_checkpoint(backend.store(), "ckpt/old", recycle=True)
     tv.save_checkpoint(rt, "ckpt/older", cps, sh, opts).wait()
-    native.mapping_quiesce()
     delete_checkpoint(backend.store(), "ckpt/older", recycle=True)
     pooled = backend.recycle_pool_bytes()
     assert pooled > 0
@@ -122,7 +121,6 @@ def test_checkpointer_recycle_loop(shm_dir, monkeypatch):
         for t in shards.values():
             t.fill_(float(step))
         ck.save_step(step, {"m": {"w": leaf}}, {"m": {"w": s}})
-        native.mapping_quiesce()
     ck.close()  # joins the save and the background retention, drains the pool
     assert ck.all_steps() == [8, 9]
     assert backend.recycle_pool(0) is None and backend.recycle_pool(1) is None
@@ -149,11 +147,10 @@ def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
     rt = tv.SimulatedRuntime(c["process_count"], backend)
     cps = helpers.checkpointables(tree, specs, rt)
     sh = helpers.shardings_for(tree, specs)
-    for i in range(4):  # fresh, recycled (queued for registration), then registered
+    for i in range(4):  # fresh, recycled (registered at this claim), then registered
         before = native.totals()["save"]
         tv.save_checkpoint(rt, "ckpt/run", cps, sh, tv.SaveOptions(**c["options"])).wait()
         after = native.totals()["save"]
-        native.mapping_quiesce()
         got = {k: v for k, v in helpers.dump_digests(backend).items() if not k.startswith(".tvpool")}
         assert got == {k: (r["size"], r["sha256"]) for k, r in gold["files"].items()}
         if i >= 2:
