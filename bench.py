@@ -1373,6 +1373,11 @@ def verify_restore(tv, state, out, leaves=None, seed: int = 0) -> tuple[int, int
         for path, leaf in tv.flatten(tree):
             ref = src[path]
             if not hasattr(leaf, "shards") or not hasattr(ref, "shards"):
+                if hasattr(leaf, "data") and hasattr(ref, "data") and hasattr(leaf.data, "is_cuda"):
+                    a, b = leaf.data, ref.data.to(leaf.data.device)  # unsharded (C1): whole arrays
+                    a, b = a.view(ints[a.element_size()]), b.view(ints[b.element_size()])
+                    compared += a.numel() * a.element_size()
+                    bad += 0 if torch.equal(a, b) else 1
                 continue
             t_ranges = leaf.shard_ranges()
             ref_ranges = ref.shard_ranges()
