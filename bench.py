@@ -565,16 +565,23 @@ def run_ours(args) -> dict:
                                   "best of 2; write = " + ("rewrite of existing files (recycling on)"
                                                            if args.recycle else "fresh files"))
     d.barrier()  # every rank probes its own link at the same time: the aggregate is concurrent
-    # one warm-up + one timed 4 GiB copy per direction, all ranks at once: long enough that
-    # every rank's copies overlap (best of 3 x 1 GiB let a rank time a copy that ran
+    # 3 rounds of (one warm-up + one timed 4 GiB copy per direction), every rank at once
+    # after a barrier, mean of the rounds: the ranks' copies overlap, so the sum over ranks
+    # is what the GPUs get concurrently (best of 3 x 1 GiB let a rank time a copy that ran
     # partly alone, overstating the aggregate)
-    d2h, h2d = native.probe_pcie(d.local if d.on else 0, 4 << 30, 1)
+    rounds = []
+    for _ in range(3):
+        d.barrier()
+        rounds.append(native.probe_pcie(d.local if d.on else 0, 4 << 30, 1))
+    d2h = statistics.mean(r[0] for r in rounds)
+    h2d = statistics.mean(r[1] for r in rounds)
     probe["pcie_d2h_GBps_per_gpu"] = round(d2h, 2)
     probe["pcie_h2d_GBps_per_gpu"] = round(h2d, 2)
     if d.on:
         probe["pcie_d2h_GBps_aggregate"] = round(d.sum(d2h), 2)
         probe["pcie_h2d_GBps_aggregate"] = round(d.sum(h2d), 2)
-        probe["pcie_aggregate_how"] = "all ranks' pinned 4 GiB D2H / H2D measured concurrently, summed"
+        probe["pcie_aggregate_how"] = ("all ranks' pinned 4 GiB D2H / H2D copies at once after a barrier, "
+                                       "mean of 3 rounds per rank, summed over ranks")
     else:
         probe["pcie_d2h_GBps_aggregate"] = round(d2h * N, 2)
         probe["pcie_h2d_GBps_aggregate"] = round(h2d * N, 2)
