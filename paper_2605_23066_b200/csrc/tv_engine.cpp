@@ -437,6 +437,12 @@ struct DeviceCtx {
   int device = -1;
   std::vector<cudaStream_t> streams;
   cudaStream_t zero_copy = nullptr;  // DMA straight into / out of registered file pages
+  // packed zero-copy: strided boxes are packed here, then DMA'd into the registered file
+  // (a small ring of its own: the save path's staging is indexed by pinned slot)
+  char* zc_ring = nullptr;
+  std::vector<cudaEvent_t> zc_ev;
+  std::vector<char> zc_used;
+  int zc_next = 0;
   std::unique_ptr<JobUploader> uploader;
   std::unique_ptr<StagingPool> staging;
   cudaStream_t stream_for(int64_t k) const { return streams[(size_t)(k % (int64_t)streams.size())]; }
@@ -763,8 +769,7 @@ class SaveRun {
     for (int i = 0; i < n_items_; ++i) {
       const auto& it = items_[i];
       const int64_t n = box_bytes(it.ext, it.rank, it.itemsize);
-      int64_t boff = 0, bn = 0;
-      if (n > 0 && outs_[it.file].mapped && box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn)) {
+      if (n > 0 && outs_[it.file].mapped) {  // contiguous: one DMA; strided: pack + DMA
         direct_[i] = 1;
         zq_.push_back(i);
       }
@@ -784,6 +789,76 @@ class SaveRun {
     std::lock_guard<std::mutex> g(zq_m_);
     if (zlo_ >= zhi_) return false;
     *i = zq_[--zhi_];
+    return true;
+  }
+
+  // D2H of `n` contiguous device bytes into a registered file mapping at `file_off`,
+  // never across a registration piece.
+  bool dma_into_file(const char* src, char* mapped, int64_t file_off, int64_t n, cudaStream_t st) {
+    for (int64_t a = 0; a < n;) {
+      const int64_t at = file_off + a;
+      const int64_t k = std::min(n - a, (at / kRegisterPiece + 1) * kRegisterPiece - at);
+      if (cudaMemcpyAsync(mapped + at, src + a, k, cudaMemcpyDefault, st) != cudaSuccess) return false;
+      a += k;
+    }
+    return true;
+  }
+
+  // A strided box (e.g. a replica-parallel column segment): packed by the box-copy kernel
+  // into a staging chunk of the device's zero-copy ring, then DMA'd into the file, chunk by
+  // chunk in payload order (split_box keeps the file contiguous), all on the zero-copy
+  // stream; a ring chunk is reused after its DMA's event.
+  bool pack_into_file(const tv_write_item& it, DeviceCtx* ctx) {
+    constexpr int kChunks = 4;
+    const int64_t chunk = kRegisterPiece;
+    if (!ctx->zc_ring) {
+      if (cudaMalloc(&ctx->zc_ring, kChunks * chunk) != cudaSuccess) {
+        err_.set(TV_ERR_NOMEM, "zero-copy pack ring");
+        return false;
+      }
+      ctx->zc_ev.assign(kChunks, nullptr);
+      ctx->zc_used.assign(kChunks, 0);
+      for (auto& ev : ctx->zc_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    }
+    std::vector<SubBox> subs;
+    split_box(it.src.off, it.ext, it.rank, it.itemsize, chunk, subs);
+    int64_t pos = it.file_off;
+    for (const SubBox& sb : subs) {
+      const int slot = ctx->zc_next;
+      ctx->zc_next = (slot + 1) % kChunks;
+      if (ctx->zc_used[slot]) cudaEventSynchronize(ctx->zc_ev[slot]);
+      char* stage = ctx->zc_ring + (int64_t)slot * chunk;
+      tv_copy cp{};
+      cp.src = it.src;
+      std::memcpy(cp.src.off, sb.off, sizeof(int64_t) * it.rank);
+      std::memcpy(cp.ext, sb.ext, sizeof(int64_t) * it.rank);
+      cp.rank = it.rank;
+      cp.itemsize = it.itemsize;
+      cp.dst.base = reinterpret_cast<uint64_t>(stage);
+      for (int d = 0; d < it.rank; ++d) {
+        cp.dst.shape[d] = sb.ext[d];
+        cp.dst.off[d] = 0;
+      }
+      std::vector<CopyJob> jobs;
+      std::string why;
+      if (!normalize(cp, jobs, why)) {
+        err_.set(TV_ERR_ARG, "pack: " + why);
+        return false;
+      }
+      int64_t launches = 0;
+      int rc = ctx->uploader->run(jobs, ctx->zero_copy, &launches);
+      if (rc != TV_OK) {
+        err_.set(rc, get_error());
+        return false;
+      }
+      stats_launches_ += launches;
+      stats_bytes_packed_ += sb.nbytes;
+      if (!dma_into_file(stage, outs_[it.file].mapped, pos, sb.nbytes, ctx->zero_copy) ||
+          cudaEventRecord(ctx->zc_ev[slot], ctx->zero_copy) != cudaSuccess)
+        return false;
+      ctx->zc_used[slot] = 1;
+      pos += sb.nbytes;
+    }
     return true;
   }
 
@@ -828,16 +903,14 @@ class SaveRun {
       }
       cudaSetDevice(it.device);
       int64_t boff = 0, bn = 0;
-      box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn);
-      const char* src = reinterpret_cast<const char*>(it.src.base) + boff;
       cudaEvent_t ev;
       bool ok = true;
-      for (int64_t a = 0; a < bn && ok;) {  // never across a registration piece
-        const int64_t at = it.file_off + a;
-        const int64_t n = std::min(bn - a, (at / kRegisterPiece + 1) * kRegisterPiece - at);
-        ok = cudaMemcpyAsync(outs_[it.file].mapped + at, src + a, n, cudaMemcpyDefault, ctx->zero_copy) ==
-             cudaSuccess;
-        a += n;
+      if (box_contiguous(it.src, it.ext, it.rank, it.itemsize, &boff, &bn)) {
+        ok = dma_into_file(reinterpret_cast<const char*>(it.src.base) + boff, outs_[it.file].mapped,
+                           it.file_off, bn, ctx->zero_copy);
+      } else {
+        bn = box_bytes(it.ext, it.rank, it.itemsize);
+        ok = pack_into_file(it, ctx);
       }
       if (!ok || cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventRecord(ev, ctx->zero_copy) != cudaSuccess) {
@@ -1607,6 +1680,8 @@ int engine_destroy(tv_engine* e) {
       cudaSetDevice(kv.first);
       for (cudaStream_t st : kv.second->streams) cudaStreamSynchronize(st);
       if (kv.second->zero_copy) cudaStreamSynchronize(kv.second->zero_copy);
+      for (auto ev : kv.second->zc_ev) cudaEventDestroy(ev);
+      if (kv.second->zc_ring) cudaFree(kv.second->zc_ring);
       kv.second->uploader.reset();
       kv.second->staging.reset();
       for (cudaStream_t st : kv.second->streams) cudaStreamDestroy(st);

@@ -130,8 +130,9 @@ def test_checkpointer_recycle_loop(shm_dir, monkeypatch):
         assert np.all(out["m"]["w"].data == float(step))
 
 
+@pytest.mark.parametrize("name", ["fsdp4_per_leaf", "replica_parallel", "fsdp4_aggregated"])
 @pytest.mark.parametrize("path", ["zero_copy", "slots"])
-def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
+def test_both_save_paths_over_recycled_files(path, name, shm_dir, monkeypatch):
     """The adaptive save-path choice may pick either path for a recycled save: both
     write the reference's bytes."""
     import paper_2605_23066_b200 as tv
@@ -140,8 +141,8 @@ def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
 
     monkeypatch.setenv("TVGPU_SAVE_PATH", path)
     monkeypatch.setenv("TVGPU_REGISTER_BUDGET", "1.0")
-    c = cases.case("fsdp4_per_leaf")
-    gold = json.loads((GOLDEN / "fsdp4_per_leaf.json").read_text())
+    c = cases.case(name)  # replica_parallel: strided segments, packed into the file (zero-copy)
+    gold = json.loads((GOLDEN / f"{name}.json").read_text())
     tree, specs = cases.build_inputs(c)
     backend = tv.FilesystemBackend(shm_dir, register_pool=True)
     rt = tv.SimulatedRuntime(c["process_count"], backend)
@@ -149,7 +150,7 @@ def test_both_save_paths_over_recycled_files(path, shm_dir, monkeypatch):
     sh = helpers.shardings_for(tree, specs)
     for i in range(4):  # fresh, recycled (registered at this claim), then registered
         before = native.totals()["save"]
-        tv.save_checkpoint(rt, "ckpt/run", cps, sh, tv.SaveOptions(**c["options"])).wait()
+        tv.save_checkpoint(rt, "ckpt/run", cps, sh, tv.SaveOptions(**c["options"], sync=i % 2 == 0)).wait()
         after = native.totals()["save"]
         got = {k: v for k, v in helpers.dump_digests(backend).items() if not k.startswith(".tvpool")}
         assert got == {k: (r["size"], r["sha256"]) for k, r in gold["files"].items()}
