@@ -76,7 +76,9 @@ def _globals(seed: int) -> dict:
 
 def _stored_digests(root: str) -> dict:
     out = {}
-    for dirpath, _, names in os.walk(root):
+    for dirpath, dirs, names in os.walk(root):
+        if ".tvpool" in dirs:
+            dirs.remove(".tvpool")  # the recycle pool holds no checkpoint files
         for n in names:
             full = os.path.join(dirpath, n)
             with open(full, "rb") as f:
@@ -164,19 +166,29 @@ def _neutral(glob, axes, P, replica_axis):
 
 
 @pytest.mark.parametrize("replica_parallel", [True, False])
-def test_c3_replica_mesh_at_size_matches_oracle(sample, replica_parallel):
+def test_c3_replica_mesh_at_size_matches_oracle(sample, replica_parallel, monkeypatch):
+    """Saved three times over recycled files (fresh; claimed + registered; zero-copy: the
+    strided segments packed into the registered files); the last one is compared."""
     import torch
 
     import paper_2605_23066_b200 as tv
+    from paper_2605_23066_b200 import native
+    from paper_2605_23066_b200.training_manager import delete_checkpoint
 
+    monkeypatch.setenv("TVGPU_SAVE_PATH", "zero_copy")
     axes, P, ra = [("replica", 2), ("fsdp", 4)], 8, "replica"
     root = _fresh("/dev/shm/tv_c3_at_size")
     try:
-        backend = tv.FilesystemBackend(root)
+        backend = tv.FilesystemBackend(root, register_pool=True)
         rt = tv.SimulatedRuntime(P, backend, gpus=_gpus(P))
         state, shardings = _sharded_tree(tv, rt, sample, axes, P, ra)
-        tv.save_checkpoint(rt, "ck", state, shardings,
-                           tv.SaveOptions(replica_parallel=replica_parallel, sync=True)).wait()
+        opts = tv.SaveOptions(replica_parallel=replica_parallel, sync=True)
+        for name in ("a", "b"):
+            tv.save_checkpoint(rt, name, state, shardings, opts).wait()
+            delete_checkpoint(backend.store(), name, recycle=True)
+        before = native.totals()["save"]["zero_copy_bytes"]
+        tv.save_checkpoint(rt, "ck", state, shardings, opts).wait()
+        assert native.totals()["save"]["zero_copy_bytes"] > before
         del state
         torch.cuda.empty_cache()
         tree, specs = _neutral(sample, axes, P, ra)
@@ -192,6 +204,7 @@ def test_c3_replica_mesh_at_size_matches_oracle(sample, replica_parallel):
             assert meta["state/params/embed"]["write_chunk"] == [16032, 4096]
         _compare_with_oracle(root, expected)
     finally:
+        native.lib().tv_mapping_release_all()
         shutil.rmtree(root, ignore_errors=True)
 
 
