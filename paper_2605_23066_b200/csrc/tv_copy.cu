@@ -128,6 +128,41 @@ __device__ __forceinline__ void copy_segment(const CopyJob& j, int64_t local_blo
   }
 }
 
+// Mode 2: mid-length runs (< kSegVecs / 2 vectors).  One warp copies a group of
+// consecutive runs along dim 0 (≤ kSegVecs vectors in all), so every lane still keeps up
+// to kUnroll loads in flight — a warp per run left one per lane on 512-byte runs (0.51 of
+// a 2-D tensor-map TMA pack, profiles/r02_tma2d_pack_probe.jsonl; with groups 0.92, and
+// above TMA on 128-byte runs: r02_box_copy_group_mode_ab.jsonl).  The group origin is
+// decomposed once; runs inside it are ss[0] / ds[0] apart.
+template <int V>
+__device__ __forceinline__ void copy_group(const CopyJob& j, int64_t local_block) {
+  using T = typename VecT<V>::T;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int vpr = (int)(j.run / V);
+  const int64_t per_row = (j.n[0] + j.group - 1) / j.group;
+  const int64_t unit = local_block * kWarps + warp;
+  const int64_t outer = unit / per_row;
+  if (outer >= j.n[1] * j.n[2]) return;
+  const int64_t first = (unit - outer * per_row) * j.group;
+  const int64_t left = j.n[0] - first;
+  const int nv = (int)(left < j.group ? left : j.group) * vpr;
+  const int64_t i1 = outer % j.n[1], i2 = outer / j.n[1];
+  const char* src = j.src + first * j.ss[0] + i1 * j.ss[1] + i2 * j.ss[2];
+  char* dst = j.dst + first * j.ds[0] + i1 * j.ds[1] + i2 * j.ds[2];
+  T buf[kUnroll];
+#pragma unroll
+  for (int k = 0; k < kUnroll; ++k) {
+    const int idx = lane + 32 * k, q = idx / vpr;
+    if (idx < nv) buf[k] = ld_stream(reinterpret_cast<const T*>(src + q * j.ss[0]) + (idx - q * vpr));
+  }
+#pragma unroll
+  for (int k = 0; k < kUnroll; ++k) {
+    const int idx = lane + 32 * k, q = idx / vpr;
+    if (idx < nv) reinterpret_cast<T*>(dst + q * j.ds[0])[idx - q * vpr] = buf[k];
+  }
+}
+
 // Mode 1: short runs; each thread decomposes its own vector indices.
 template <int V>
 __device__ __forceinline__ void copy_flat(const CopyJob& j, int64_t local_block) {
@@ -159,6 +194,8 @@ template <int V>
 __device__ __forceinline__ void dispatch_mode(const CopyJob& j, int64_t local_block) {
   if (j.mode == 0)
     copy_segment<V>(j, local_block);
+  else if (j.mode == 2)
+    copy_group<V>(j, local_block);
   else
     copy_flat<V>(j, local_block);
 }
@@ -278,7 +315,19 @@ bool normalize(const tv_copy& c, std::vector<CopyJob>& out, std::string& err) {
     }
     j.nruns = j.n[0] * j.n[1] * j.n[2];
     j.vec = vec_width(g);
-    j.mode = (run / j.vec >= 32) ? 0 : 1;
+    // ≥ 2 KiB-class runs: a warp per run segment; shorter ones: a warp per group of runs
+    // when a group fills at least two vectors per lane; else flat (or a warp per run)
+    const int64_t vpr = run / j.vec;
+    const int64_t group = std::min<int64_t>(j.n[0], kSegVecs / std::max<int64_t>(vpr, 1));
+    j.group = 1;
+    if (vpr >= kSegVecs / 2) {
+      j.mode = 0;
+    } else if (group * vpr >= 64) {
+      j.mode = 2;
+      j.group = (int32_t)group;
+    } else {
+      j.mode = vpr >= 32 ? 0 : 1;
+    }
     out.push_back(j);
   }
   return true;
@@ -291,6 +340,9 @@ int64_t plan_units(std::vector<CopyJob>& jobs) {
     if (j.mode == 0) {
       const int64_t segs = (vpr + kSegVecs - 1) / kSegVecs;
       j.units = (j.nruns * segs + kWarps - 1) / kWarps;
+    } else if (j.mode == 2) {
+      const int64_t groups = j.n[1] * j.n[2] * ((j.n[0] + j.group - 1) / j.group);
+      j.units = (groups + kWarps - 1) / kWarps;
     } else {
       j.units = (j.nruns * vpr + kFlatVecs - 1) / kFlatVecs;
     }

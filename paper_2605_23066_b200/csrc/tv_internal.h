@@ -51,7 +51,9 @@ struct CopyJob {
   int64_t units;      // work units of this job (see kernel)
   int64_t unit_begin; // prefix sum of units over the batch
   int32_t vec;        // vector width in bytes (1,2,4,8,16)
-  int32_t mode;       // 0 = warp per run segment, 1 = flat (short runs)
+  int32_t mode;       // 0 = warp per run segment, 1 = flat (short runs), 2 = warp per run group
+  int32_t group;      // mode 2: consecutive runs of dim 0 per warp unit
+  int32_t pad_;
 };
 
 // Split a tv_copy into canonical jobs (appends; returns false on malformed input).

@@ -47,6 +47,40 @@ def test_random_boxes_all_ranks_and_itemsizes():
         assert torch.equal(dst, expect), (case, sshape, ext, soff, dshape, doff, isz)
 
 
+@pytest.mark.parametrize("run_bytes", [16, 48, 128, 496, 512, 1008, 1024, 2032, 2048, 4096])
+def test_run_groups_every_mode(run_bytes):
+    """Runs from one vector to 4 KiB (the warp-per-group mode covers < 2 KiB runs; flat
+    and warp-per-segment the rest), dim-0 extents that do and do not divide the group,
+    three outer dims plus host-enumerated ones, 16-byte and misaligned bases."""
+    import torch
+
+    from paper_2605_23066_b200 import native
+
+    rng = random.Random(run_bytes)
+    for case in range(6):
+        n0 = rng.choice([1, 2, 3, 7, 31, 64, 129, 300])
+        outer = tuple(rng.randint(1, 4) for _ in range(rng.randint(0, 4)))
+        isz = rng.choice([1, 2, 4, 8]) if run_bytes % 8 == 0 else 1
+        tdt = getattr(torch, DT[isz])
+        cols = run_bytes // isz
+        ext = outer + (n0, cols)
+        sshape = tuple(e + rng.randint(0, 2) for e in outer) + (n0 + rng.randint(0, 3), cols + rng.choice([0, 8, 40]))
+        dshape = tuple(e + rng.randint(0, 2) for e in ext[:-1]) + (cols + rng.choice([0, 16]),)
+        soff = tuple(rng.randint(0, s - e) for s, e in zip(sshape, ext))
+        doff = tuple(rng.randint(0, d - e) for d, e in zip(dshape, ext))
+        shift = (0, 0) if case % 2 == 0 else (isz, 0)
+        numel = int(np.prod(sshape))
+        flat = torch.randint(0, 100, (numel + 1,), dtype=tdt, device="cuda")
+        src = flat[:numel].view(sshape)
+        seen = flat[1:].view(sshape) if shift[0] else src  # what a base one element on reads
+        dst = torch.zeros(dshape, dtype=tdt, device="cuda")
+        expect = dst.clone()
+        expect[tuple(slice(o, o + e) for o, e in zip(doff, ext))] = \
+            seen[tuple(slice(o, o + e) for o, e in zip(soff, ext))]
+        _copy(native, torch, src, soff, dst, doff, ext, isz, shift)
+        assert torch.equal(dst, expect), (run_bytes, case, sshape, ext, soff, dshape, doff, isz, shift)
+
+
 def test_misaligned_bases_fall_back_to_narrow_vectors():
     import torch
 
