@@ -739,6 +739,8 @@ def run_ours(args) -> dict:
         torch.cuda.empty_cache()
         c5 = c5_loop(tv, d, rt, N, base, args.c5_layers, args.c5_steps, args.train_ms, recycle=args.recycle)
         free_recycle_pool(native, d, backend)
+    c3 = (c3_leg(tv, native, d, rt, backend, args, N, base)
+          if args.c3_steps > 0 and wl.name == "c2" and N >= 4 and N % 2 == 0 else None)
     c1 = c1_leg(tv, native, d, base, args) if args.c1_steps > 0 and wl.name == "c2" else None
 
     peaks = measured_peaks()
@@ -803,6 +805,7 @@ def run_ours(args) -> dict:
         "e2e": e2e,
         "c5": c5,
         "c1": c1,
+        "c3": c3,
         "reshard": reshard,
         "gpu_launches": int(kernels),
         "gpu_launches_breakdown": {
@@ -1215,6 +1218,77 @@ def retire_checkpoint(d, backend, path: str, recycle: bool) -> None:
     d.barrier()
     if d.rank == 0:
         delete_checkpoint(store, path, recycle=recycle)
+
+
+def c3_leg(tv, native, d, rt, backend, args, N: int, base: str) -> dict:
+    """BASELINE configs[2] in the default line at N >= 4 (N = 8 is its 2 x 4 mesh, P = 8):
+    the same tree on a (replica 2 x fsdp N/2) mesh, replica-parallel save (each replica
+    GPU writes 1/2 of its shard) + restore onto the same mesh, the step's save mode,
+    recycled + registered files like the main loop.  Timed like the step (CUDA events,
+    barrier + sync, max over ranks); the last restore is verified on the device."""
+    import dataclasses
+
+    import torch
+
+    leaves = llama_leaves(**dict(LLAMA3_8B, layers=args.layers))
+    tree_bytes = sum(nbytes(s, dt) for _, _, s, dt in leaves)
+    mesh = tv.Mesh.create([("replica", 2), ("fsdp", N // 2)], process_count=N, replica_axis="replica")
+    target = f"2x{N // 2} (replica x fsdp), {N} processes, replica-parallel save"
+    # state + restored copy (+ the async snapshot arena) per GPU, each 2 x tree / N
+    per_gpu = 2 * tree_bytes // N * (3 if args.save_mode == "async" else 2)
+    dev = d.local if d.on else 0
+    free = torch.cuda.mem_get_info(dev)[0] + torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    if d.max(-free) > -(per_gpu + (4 << 30)):
+        return {"target": target, "skipped": f"needs {per_gpu / 1e9:.1f} GB of free HBM per GPU"}
+    state, shardings = build_state(tv, rt, mesh, leaves, seed=3, spec_fn=fsdp_spec)
+    opts = tv.SaveOptions(sync=args.save_mode == "sync", replica_parallel=True, layout=args.layout)
+    backend.register_pool = bool(args.recycle) and not args.no_register
+    saves, restores, verified = [], [], {}
+    warm = 3
+    for i in range(warm + args.c3_steps):
+        path = f"bench/c3_{i}"
+        d.barrier()
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        tv.save_checkpoint(rt, path, state, shardings, opts).wait()
+        e1.record()
+        out = tv.load_checkpoint(rt, path, None, tv.LoadOptions(), current_mesh=mesh)
+        e2.record()
+        torch.cuda.synchronize()
+        if i >= warm:
+            saves.append(d.max(e0.elapsed_time(e1)))
+            restores.append(d.max(e1.elapsed_time(e2)))
+        if i == warm + args.c3_steps - 1:
+            nb, bad = verify_restore(tv, state, out, leaves, seed=3)
+            verified = {"bytes_compared": int(d.sum(nb)), "mismatched_boxes": int(d.sum(bad))}
+        del out
+        d.barrier()
+        retire_checkpoint(d, backend, path, args.recycle)
+        if d.rank == 0:
+            shutil.rmtree(os.path.join(base, path), ignore_errors=True)
+        d.barrier()
+    del state
+    backend.register_pool = False
+    free_recycle_pool(native, d, backend)
+    torch.cuda.empty_cache()
+    save_ms, restore_ms = statistics.mean(saves), statistics.mean(restores)
+    return {
+        "target": target,
+        "GBps": round(2 * tree_bytes / ((save_ms + restore_ms) / 1e3) / 1e9, 3),
+        "save_GBps": round(tree_bytes / (save_ms / 1e3) / 1e9, 3),
+        "restore_GBps": round(tree_bytes / (restore_ms / 1e3) / 1e9, 3),
+        "save_ms": round(save_ms, 2),
+        "restore_ms": round(restore_ms, 2),
+        "steps": args.c3_steps,
+        "warmup": warm,
+        "tree_bytes": tree_bytes,
+        "restore_verified": dict(verified, how="every restored shard (both replicas) against the saved "
+                                               "state, torch.equal on the device (all ranks)"),
+        "note": "GB/s counts the tree once per save and once per restore (as the metric); the "
+                "restore lands 2 x tree bytes in HBM (both replicas; stored chunks read once, "
+                "fanned out over NVLink)",
+    }
 
 
 def c1_leg(tv, native, d, base: str, args) -> dict | None:
@@ -1725,6 +1799,9 @@ def main() -> None:
     ap.add_argument("--c5-layers", type=int, default=8,
                     help="default line: Llama depth of the embedded C5 Checkpointer loop (0 = skip)")
     ap.add_argument("--c5-steps", type=int, default=20)
+    ap.add_argument("--c3-steps", type=int, default=3,
+                    help="C3 leg of the default line at N >= 4 (replica 2 x fsdp N/2, replica-parallel "
+                         "save + restore; 0 = skip)")
     ap.add_argument("--c1-steps", type=int, default=10,
                     help="default line: C1 (4 x 64 MiB f32, one process) round trips after the C2 legs (0 = skip)")
     ap.add_argument("--c1-warmup", type=int, default=3)
