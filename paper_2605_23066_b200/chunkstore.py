@@ -29,7 +29,7 @@ from typing import Any, Iterable, Iterator, Optional, Sequence
 
 import numpy as np
 
-from . import docio
+from . import docio, gcpolicy
 from .backend import Store
 from .dtypes import itemsize, numpy_dtype
 from .errors import (
@@ -1089,6 +1089,9 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     copies = native.copy_table(cols["sb"], cols["ss"], cols["so"], cols["db"], cols["ds"], cols["do"],
                                cols["ext"], cols["isz"], cols["sdt"], cols["ddt"], cols["flg"])
     with native.engine_lease(cfg, concurrent) as eng:
+        # a restore planned with the collector paused runs the pending pass behind the
+        # engine call (GIL released there), not before or after it
+        gcpolicy.collect_behind(int(ritems["nbytes"].sum()))
         stats = eng.load(ritems, inputs, copies)
     native.account_peer(peer_bytes)
     backend.record_bulk(

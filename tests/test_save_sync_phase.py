@@ -50,6 +50,30 @@ def test_gc_paused_keeps_a_disabled_collector_disabled():
         gc.enable()
 
 
+def test_collect_behind_runs_a_pass_on_the_helper_thread_for_large_restores():
+    import time
+
+    from paper_2605_23066_b200 import gcpolicy
+
+    c = gcpolicy._COLLECTOR
+    before = c.passes
+    with gcpolicy.paused():
+        assert not gcpolicy.collect_behind(gcpolicy.COLLECT_BEHIND_BYTES - 1)  # too short to hide
+        assert gcpolicy.collect_behind(gcpolicy.COLLECT_BEHIND_BYTES)
+        deadline = time.time() + 10
+        while c.passes == before and time.time() < deadline:
+            time.sleep(0.01)
+        assert c.passes > before
+        assert not gc.isenabled()  # the pass does not re-enable the paused collector
+    assert gc.isenabled()
+    gc.disable()
+    try:  # a caller that disabled the collector keeps it off: no passes behind its back
+        with gcpolicy.paused():
+            assert not gcpolicy.collect_behind(gcpolicy.COLLECT_BEHIND_BYTES)
+    finally:
+        gc.enable()
+
+
 def test_caller_streams_without_gpu():
     class RT:
         gpus = [0]
