@@ -29,7 +29,7 @@ from typing import Any, Iterable, Iterator, Optional, Sequence
 
 import numpy as np
 
-from . import docio, gcpolicy
+from . import docio
 from .backend import Store
 from .dtypes import itemsize, numpy_dtype
 from .errors import (
@@ -996,9 +996,11 @@ def _within_staging(items: list[FetchItem], budget: int) -> list[FetchItem]:
     return out
 
 
-def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurrent: int = 1):
+def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurrent: int = 1,
+                  before_engine=None):
     """Fetch every item once onto its reader GPU and scatter it into every consumer
-    (local or peer GPUs).  Admission / recording of the get ops as in execute_writes."""
+    (local or peer GPUs).  Admission / recording of the get ops as in execute_writes.
+    ``before_engine(nbytes)`` runs right before the blocking engine call."""
     from . import native
 
     if not items:
@@ -1089,9 +1091,8 @@ def execute_reads(store: Store, items: list[FetchItem], engine_cfg=None, concurr
     copies = native.copy_table(cols["sb"], cols["ss"], cols["so"], cols["db"], cols["ds"], cols["do"],
                                cols["ext"], cols["isz"], cols["sdt"], cols["ddt"], cols["flg"])
     with native.engine_lease(cfg, concurrent) as eng:
-        # a restore planned with the collector paused runs the pending pass behind the
-        # engine call (GIL released there), not before or after it
-        gcpolicy.collect_behind(int(ritems["nbytes"].sum()))
+        if before_engine is not None:
+            before_engine(int(ritems["nbytes"].sum()))
         stats = eng.load(ritems, inputs, copies)
     native.account_peer(peer_bytes)
     backend.record_bulk(

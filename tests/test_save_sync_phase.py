@@ -94,3 +94,23 @@ def test_reference_defaults_switch_load_options():
     finally:
         reference_defaults(False)
     assert LoadOptions().to_host is False
+
+
+def test_restore_requests_the_gc_pass_when_its_last_thread_enters_the_engine(monkeypatch):
+    """Threads runtime: every local restoring thread announces its engine call; only the
+    last one requests the pass (an earlier request would stall the others' table
+    building behind the GIL-holding collector)."""
+    import types
+
+    from paper_2605_23066_b200 import gcpolicy
+    from paper_2605_23066_b200.load_pipeline import _RestoreJob
+
+    calls = []
+    monkeypatch.setattr(gcpolicy, "collect_behind", lambda n: calls.append(n) or True)
+    job = types.SimpleNamespace(lock=threading.Lock(), engine_entries=0, engine_bytes=0,
+                                local_processes={0, 1, 2},
+                                items_by_process={0: ["a"], 1: ["b"], 2: [], 3: ["remote"]})
+    _RestoreJob.entering_engine(job, 6 << 30)
+    assert calls == []
+    _RestoreJob.entering_engine(job, 2 << 30)
+    assert calls == [4 << 30]  # mean bytes per busy local process
