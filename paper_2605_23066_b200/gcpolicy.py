@@ -4,9 +4,11 @@ A gen-2 pass over a training process's heap costs tens of milliseconds (measured
 restore planning: 38-42 ms of a 47-55 ms phase, ``profiles/r02_gc_sources_n{2,4}.json``).
 The save's synchronous phase and the restore's planning run with the collector paused
 (``paused``); a large restore then has the pending collection run on a helper thread
-while the calling thread waits in the native engine (``collect_behind``, requested right
-before the blocking engine call: the pass holds the GIL, so any Python work after the
-request waits for it), so the pass overlaps the DMA instead of preceding it."""
+while the calling threads wait in the native engine (``collect_behind``, requested right
+before the blocking engine call by the last local restoring thread to get there,
+``_RestoreJob.entering_engine``: the pass holds the GIL, so any Python work after the
+request waits for it), so the pass overlaps the DMA instead of preceding it
+(``profiles/r02_ab_gc_policy_n{1,4}.jsonl``)."""
 
 from __future__ import annotations
 
