@@ -1082,16 +1082,18 @@ def time_launch(fn, gpu: int, reps: int = 5, warmup: int = 3) -> tuple[float, fl
 
 def _ncu_traffic(bytes_per_launch: int):
     """DRAM bytes per launch of the same kernel launch from a committed ncu capture
-    (profiles/r01_roofline_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum),
-    used only when that capture's launch moved exactly the bytes this one did."""
-    path = os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")
-    if not os.path.exists(path):
-        return None, None
-    with open(path) as f:
-        rows = json.load(f).get("launches", [])
-    for r in rows:
-        if int(r["algorithmic_bytes"]) == int(bytes_per_launch):
-            return int(r["dram_read_bytes"]) + int(r["dram_write_bytes"]), r.get("source")
+    (dram__bytes_read.sum + dram__bytes_write.sum; the current build's capture first,
+    profiles/r02_roofline_traffic_full.json, then round 1's), used only when that
+    capture's launch moved exactly the bytes this one did."""
+    for name in ("r02_roofline_traffic_full.json", "r01_roofline_traffic.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        if not os.path.exists(path):
+            continue
+        with open(path) as f:
+            rows = json.load(f).get("launches", [])
+        for r in rows:
+            if int(r["algorithmic_bytes"]) == int(bytes_per_launch):
+                return int(r["dram_read_bytes"]) + int(r["dram_write_bytes"]), f"{r.get('source')} [{name}]"
     return None, None
 
 
