@@ -136,6 +136,7 @@ int main() {
       {"contiguous_4096_of_4096", 131072, 4096, 4096},  // one run (the snapshot), 1 GiB out
       {"q_o_2048_of_4096", 65536, 4096, 2048},      // 4 KiB runs, 256 MiB out
       {"down_7168_of_14336", 16384, 14336, 7168},   // 14 KiB runs, 224 MiB out
+      {"tp_1024_of_4096", 65536, 4096, 1024},       // 2 KiB runs, 128 MiB out
       {"tp_512_of_4096", 131072, 4096, 512},        // 1 KiB runs, 128 MiB out
       {"tp_256_of_4096", 262144, 4096, 256},        // 512 B runs, 128 MiB out
       {"tp_64_of_4096", 1048576, 4096, 64},         // 128 B runs, 128 MiB out
