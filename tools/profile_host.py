@@ -1,7 +1,8 @@
-"""Host-side (Python) cost of one save, one restore and one retire of the C2 tree at one
-GPU (the protocol around the DMA): cProfile of each call, top functions by own time.
+"""Host-side (Python) cost of one save, one restore and one retire of the C2 tree (or,
+with --c1, of the C1 tree: 4 x (4096,4096) f32 unsharded) at one GPU (the protocol around
+the DMA): cProfile of each call, top functions by own time.
 
-    python tools/profile_host.py [--layers 32]
+    python tools/profile_host.py [--layers 32] [--c1]
 """
 
 from __future__ import annotations
@@ -22,6 +23,7 @@ sys.path.insert(0, ROOT)
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--c1", action="store_true")
     args = ap.parse_args()
     import torch
 
@@ -34,10 +36,16 @@ def main() -> None:
     backend = tv.FilesystemBackend(base)
     rt = tv.SimulatedRuntime(1, backend, gpus=[0])
     mesh = tv.Mesh.create([("fsdp", 1)], process_count=1)
-    leaves = bench.llama_leaves(**dict(bench.LLAMA3_8B, layers=args.layers))
-    state, shardings = bench.build_state(tv, rt, mesh, leaves)
+    if args.c1:
+        backend.register_pool = True  # as the bench's C1 leg
+        state = {"model": {f"a{i}": tv.DenseArray("f32", torch.randn((4096, 4096), device="cuda"))
+                           for i in range(4)}}
+        shardings, mesh = None, None
+    else:
+        leaves = bench.llama_leaves(**dict(bench.LLAMA3_8B, layers=args.layers))
+        state, shardings = bench.build_state(tv, rt, mesh, leaves)
     torch.cuda.synchronize()
-    for i in range(3):  # warm: recycle pool, registrations, plan caches
+    for i in range(6):  # warm: recycle pool, registrations, plan caches
         tv.save_checkpoint(rt, f"w{i}", state, shardings, tv.SaveOptions(sync=False)).wait()
         out = tv.load_checkpoint(rt, f"w{i}", None, tv.LoadOptions(), current_mesh=mesh)
         del out
